@@ -1,0 +1,65 @@
+"""Second, independent oracle (O2) in pure Python.  TEST INFRASTRUCTURE ONLY.
+
+Used to pin oracle/sinet_oracle.c on small inputs by methods that share none
+of its arithmetic:
+  * membership by comparing the first Z characters of 32-character binary
+    strings (the "32-bit sequence" of P:L174-175, compared bit by bit);
+  * membership by Python's ``ipaddress`` library (``ip in ip_network(c, strict=False)``);
+  * histograms with ``collections.Counter`` keyed by (dir, ms bin) (P:L217's
+    key-value namespaces X1<timestamp>, X1<count>, X2<bytes>), Python ints
+    reduced mod 2^64 only at the end.
+"""
+from __future__ import annotations
+
+import ipaddress
+from collections import Counter
+
+M64 = (1 << 64) - 1
+
+
+def bits32(x: int) -> str:
+    return format(x, "032b")
+
+
+def member_bitstring(ip: int, nets, lens) -> bool:
+    """Any CIDR whose first Z bits equal the address's first Z bits (reading A3)."""
+    s = bits32(ip)
+    return any(s[:z] == bits32(int(n))[:z] for n, z in zip(nets, lens))
+
+
+def member_ipaddress(ip: int, nets, lens) -> bool:
+    a = ipaddress.IPv4Address(int(ip))
+    return any(a in ipaddress.IPv4Network((int(n), int(z)), strict=False) for n, z in zip(nets, lens))
+
+
+def histogram_counter(ts, src, dst, nbytes, nets, lens, start, window, width, lut):
+    """Returns (count Counter, bytes Counter keyed by (dir, bin)), m_count, m_bytes, oow_count, oow_bytes."""
+    cnt, byt = Counter(), Counter()
+    m_count, m_bytes = [0] * 4, [0] * 4
+    oow_c, oow_b = [0, 0], [0, 0]
+    memo = {}
+
+    def mem(ip):
+        if ip not in memo:
+            memo[ip] = member_bitstring(ip, nets, lens)
+        return memo[ip]
+
+    for t, s, d, b in zip(ts, src, dst, nbytes):
+        t, s, d, b = int(t), int(s), int(d), int(b)
+        cell = 2 * int(mem(s)) + int(mem(d))
+        m_count[cell] += 1
+        m_bytes[cell] += b
+        direction = lut[cell]
+        if direction not in (0, 1):
+            continue
+        off = t - start
+        if off < 0 or off >= window:
+            oow_c[direction] += 1
+            oow_b[direction] += b
+            continue
+        key = (direction, off // width)
+        cnt[key] += 1
+        byt[key] += b
+    byt = Counter({k: v & M64 for k, v in byt.items()})
+    return (cnt, byt, [c & M64 for c in m_count], [c & M64 for c in m_bytes],
+            [c & M64 for c in oow_c], [c & M64 for c in oow_b])

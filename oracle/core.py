@@ -1,0 +1,155 @@
+"""ctypes wrapper of oracle/sinet_oracle.c.  TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Every function here is marshalling only; the arithmetic lives in the C file,
+which cites the paper passage each step follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sinet_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+# direction-LUT presets, index s_in*2 + d_in -> 0 OUT, 1 IN, 2 NEITHER (A1/A2)
+OUT, IN, NEITHER = 0, 1, 2
+LUT_ALG1 = (IN, IN, OUT, OUT)              # Alg. 1 literal: source decides
+LUT_SRC_PRIORITY = (NEITHER, IN, OUT, OUT)  # default
+LUT_STRICT = (NEITHER, IN, OUT, NEITHER)
+
+
+def build(force: bool = False) -> str:
+    """Compile sinet_oracle.c with plain gcc (no CUDA, no product headers)."""
+    with _lock:
+        if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+            tmp = _LIB + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread",
+                                   "-Wall", "-Wextra", "-o", tmp, _SRC])
+            os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        u64p = ctypes.POINTER(ctypes.c_uint64)
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        u8p = ctypes.POINTER(ctypes.c_uint8)
+        lib.oracle_mask.argtypes = [ctypes.c_uint32]
+        lib.oracle_mask.restype = ctypes.c_uint32
+        lib.oracle_bitmask.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+        lib.oracle_bitmask.restype = ctypes.c_uint32
+        lib.oracle_member.argtypes = [ctypes.c_uint32, u32p, u8p, ctypes.c_uint32]
+        lib.oracle_member.restype = ctypes.c_int
+        common = [u64p, u32p, u32p, u64p, ctypes.c_uint64, u32p, u8p, ctypes.c_uint32,
+                  ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, u8p, u64p, u64p, u64p]
+        lib.oracle_classify_histogram.argtypes = common
+        lib.oracle_classify_histogram.restype = None
+        lib.oracle_classify_histogram_mt.argtypes = common + [ctypes.c_int]
+        lib.oracle_classify_histogram_mt.restype = ctypes.c_int
+        lib.oracle_tags.argtypes = [u64p, u32p, u32p, ctypes.c_uint64, u32p, u8p, ctypes.c_uint32,
+                                    ctypes.c_uint64, ctypes.c_uint64, u8p]
+        lib.oracle_tags.restype = None
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def mask(z: int) -> int:
+    return int(_load().oracle_mask(z))
+
+
+def bitmask(addr: int, z: int) -> int:
+    return int(_load().oracle_bitmask(addr, z))
+
+
+def _table(nets, lens):
+    nets = np.ascontiguousarray(np.asarray(nets, dtype=np.uint32))
+    lens = np.ascontiguousarray(np.asarray(lens, dtype=np.uint8))
+    assert nets.shape == lens.shape
+    return nets, lens
+
+
+def member(ip: int, nets, lens) -> bool:
+    nets, lens = _table(nets, lens)
+    return bool(_load().oracle_member(ip, _ptr(nets, ctypes.c_uint32), _ptr(lens, ctypes.c_uint8), len(nets)))
+
+
+class OracleResult:
+    """count[dir][bin], bytes[dir][bin] (u64, dir 0 = OUT, 1 = IN) and totals[12]."""
+
+    def __init__(self, nbins: int):
+        self.nbins = nbins
+        self.count = np.zeros((2, nbins), dtype=np.uint64)
+        self.bytes = np.zeros((2, nbins), dtype=np.uint64)
+        self.totals = np.zeros(12, dtype=np.uint64)
+
+    # named views of the totals vector (layout documented in sinet_oracle.c)
+    @property
+    def m_count(self):
+        return self.totals[0:4]
+
+    @property
+    def m_bytes(self):
+        return self.totals[4:8]
+
+    @property
+    def oow_count(self):
+        return self.totals[8:10]
+
+    @property
+    def oow_bytes(self):
+        return self.totals[10:12]
+
+
+def classify_histogram(ts, src, dst, nbytes, nets, lens, start: int, window: int, width: int,
+                       lut=LUT_SRC_PRIORITY, threads: int = 1, into: OracleResult | None = None) -> OracleResult:
+    """Run the oracle over one batch of records; accumulate into ``into`` if given."""
+    lib = _load()
+    ts = np.ascontiguousarray(ts, dtype=np.uint64)
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    nbytes = np.ascontiguousarray(nbytes, dtype=np.uint64)
+    n = len(ts)
+    assert len(src) == n and len(dst) == n and len(nbytes) == n
+    assert width >= 1 and window % width == 0
+    nets, lens = _table(nets, lens)
+    lut_a = np.ascontiguousarray(np.asarray(lut, dtype=np.uint8))
+    res = into if into is not None else OracleResult(window // width)
+    assert res.nbins == window // width
+    args = (_ptr(ts, ctypes.c_uint64), _ptr(src, ctypes.c_uint32), _ptr(dst, ctypes.c_uint32),
+            _ptr(nbytes, ctypes.c_uint64), n, _ptr(nets, ctypes.c_uint32), _ptr(lens, ctypes.c_uint8),
+            len(nets), start, window, width, _ptr(lut_a, ctypes.c_uint8),
+            _ptr(res.count, ctypes.c_uint64), _ptr(res.bytes, ctypes.c_uint64),
+            _ptr(res.totals, ctypes.c_uint64))
+    if threads <= 1:
+        lib.oracle_classify_histogram(*args)
+    else:
+        rc = lib.oracle_classify_histogram_mt(*args, int(threads))
+        if rc != 0:
+            raise RuntimeError("oracle_classify_histogram_mt failed")
+    return res
+
+
+def tags(ts, src, dst, nets, lens, start: int, window: int) -> np.ndarray:
+    lib = _load()
+    ts = np.ascontiguousarray(ts, dtype=np.uint64)
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    nets, lens = _table(nets, lens)
+    out = np.zeros(len(ts), dtype=np.uint8)
+    lib.oracle_tags(_ptr(ts, ctypes.c_uint64), _ptr(src, ctypes.c_uint32), _ptr(dst, ctypes.c_uint32),
+                    len(ts), _ptr(nets, ctypes.c_uint32), _ptr(lens, ctypes.c_uint8), len(nets),
+                    start, window, _ptr(out, ctypes.c_uint8))
+    return out

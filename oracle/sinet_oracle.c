@@ -1,0 +1,203 @@
+/*
+ * sinet_oracle.c -- the plain, slow, obviously-correct CPU ORACLE for the
+ * SINET discrimination + millisecond-histogram hot path (arXiv 2106.12863).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant with the CUDA path under
+ * paper_2106_12863_b200/ and include/ (it does not include them and they do
+ * not include it).
+ *
+ * Citations: "P:Lnn" = line nn of the paper text; section numbers
+ * follow the paper.  Readings where the paper is silent or ambiguous are the
+ * A1..A23 list in DESIGN.md ("Readings").
+ *
+ * Everything is integer arithmetic; u64 sums wrap modulo 2^64 (reading A18).
+ *
+ * Pinned by tests/test_oracle_*.py against: the worked values of the paper's
+ * operations (bitmask S:L196-198 / P:L160-161), brute-force 32-character
+ * bit-string prefix comparison, Python's ipaddress module, collections.Counter
+ * histograms, the hand-derived fixture tests/golden/f0.json, closed-form
+ * invariants (conservation, permutation/chunk/shard invariance) and the
+ * generator's construction-time ground truth.
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+/* ---------------------------------------------------------------------- */
+/* Alg. 1 lines 6-7: SB = bitmask(X.X.X.X, Z), CB = bitmask(Y.Y.Y.Y, Z).
+ * "translated to a 32-bit sequence": keep the Z leading bits of
+ * the 32-bit address, clear the remaining 32-Z.  Z in [0,32] (reading A10);
+ * Z == 0 is special-cased because a C shift by 32 is undefined.             */
+uint32_t oracle_mask(uint32_t z)
+{
+    if (z == 0) return 0u;
+    return 0xFFFFFFFFu << (32u - z);
+}
+
+uint32_t oracle_bitmask(uint32_t addr, uint32_t z)
+{
+    return addr & oracle_mask(z);
+}
+
+/* Alg. 1 lines 4-9 applied to one address against the whole
+ * "CIDR list", match-any (reading A3), the block's Z masking both
+ * sides (reading A4), and "Instead of matching S.D. to C.B., we use minus at
+ * line 8": result = SB - CB in unsigned 32-bit arithmetic, a match
+ * iff result == 0 (reading A5).  Linear scan, no precompiled table.         */
+int oracle_member(uint32_t ip, const uint32_t* nets, const uint8_t* lens, uint32_t p)
+{
+    for (uint32_t i = 0; i < p; ++i) {
+        uint32_t z = lens[i];
+        uint32_t sb = oracle_bitmask(ip, z);        /* Alg.1 l.6 */
+        uint32_t cb = oracle_bitmask(nets[i], z);   /* Alg.1 l.7 (normalises host bits, A9) */
+        uint32_t result = sb - cb;                  /* Alg.1 l.8 */
+        if (result == 0u) return 1;                 /* Alg.1 l.9 */
+    }
+    return 0;
+}
+
+/* Direction codes of the output: 0 = OUT (outgoing), 1 = IN (ingoing),
+ * 2 = NEITHER (not binned, reading A20).  lut[s_in*2 + d_in] -> direction
+ * (reading A1/A2; presets ALG1 {IN,IN,OUT,OUT}, SRC_PRIORITY {NEI,IN,OUT,OUT},
+ * STRICT {NEI,IN,OUT,NEI}).                                                  */
+
+/* Totals layout (12 x u64), reading A14 and the north_star invariants:
+ *   [0..3]  m_count[s_in*2+d_in]   -- every record, mode independent
+ *   [4..7]  m_bytes[s_in*2+d_in]
+ *   [8..9]  oow_count[dir]         -- dir in {OUT, IN}, ts outside the window
+ *   [10..11] oow_bytes[dir]                                                  */
+
+/* One record through the method, in the paper's order: discriminate first
+ * ("each workload (chunk) ... is discriminated and marked as ingoing/outgoing"
+ * before the map-reduce phase), then Map to a
+ * millisecond key and Reduce by addition (P:L202-204,
+ * P:L213-214). */
+static void oracle_one(uint64_t ts, uint32_t src, uint32_t dst, uint64_t bytes,
+                       const uint32_t* nets, const uint8_t* lens, uint32_t p,
+                       uint64_t start, uint64_t window, uint32_t width,
+                       const uint8_t lut[4], uint64_t nbins,
+                       uint64_t* out_count, uint64_t* out_bytes, uint64_t* totals)
+{
+    int s_in = oracle_member(src, nets, lens, p);
+    int d_in = oracle_member(dst, nets, lens, p);
+    int cell = s_in * 2 + d_in;
+    totals[0 + cell] += 1u;
+    totals[4 + cell] += bytes;
+    int dir = lut[cell];
+    if (dir != 0 && dir != 1) return;                     /* NEITHER: not binned */
+    if (ts < start || ts - start >= window) {             /* reading A14 */
+        totals[8 + dir] += 1u;
+        totals[10 + dir] += bytes;
+        return;
+    }
+    uint64_t key = (ts - start) / (uint64_t)width;        /* Map, half-open bins (A15) */
+    out_count[(uint64_t)dir * nbins + key] += 1u;         /* <timestamp, count> */
+    out_bytes[(uint64_t)dir * nbins + key] += bytes;      /* <timestamp, bytes> */
+}
+
+/* Accumulates (does not clear) into out_count[2][nbins], out_bytes[2][nbins]
+ * and totals[12], nbins = window / width.  Records in any order.             */
+void oracle_classify_histogram(const uint64_t* ts, const uint32_t* src, const uint32_t* dst,
+                               const uint64_t* bytes, uint64_t n,
+                               const uint32_t* nets, const uint8_t* lens, uint32_t p,
+                               uint64_t start, uint64_t window, uint32_t width,
+                               const uint8_t lut[4],
+                               uint64_t* out_count, uint64_t* out_bytes, uint64_t* totals)
+{
+    uint64_t nbins = window / width;
+    for (uint64_t r = 0; r < n; ++r)
+        oracle_one(ts[r], src[r], dst[r], bytes[r], nets, lens, p, start, window, width,
+                   lut, nbins, out_count, out_bytes, totals);
+}
+
+/* Per-record tag: s_in | d_in << 1 | (ts outside window) << 2. */
+void oracle_tags(const uint64_t* ts, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                 const uint32_t* nets, const uint8_t* lens, uint32_t p,
+                 uint64_t start, uint64_t window, uint8_t* tags)
+{
+    for (uint64_t r = 0; r < n; ++r) {
+        int s_in = oracle_member(src[r], nets, lens, p);
+        int d_in = oracle_member(dst[r], nets, lens, p);
+        int oow = (ts[r] < start || ts[r] - start >= window) ? 1 : 0;
+        tags[r] = (uint8_t)(s_in | (d_in << 1) | (oow << 2));
+    }
+}
+
+/* ---------------------------------------------------------------------- */
+/* The same definition evaluated by several host threads, only to make the
+ * full-size configurations finish in seconds.  Each thread owns a contiguous
+ * slab of bins and scans every record, handling exactly the records whose
+ * bin lies in its slab; thread 0 also handles every record that is not binned
+ * (NEITHER or out of window).  Every record is therefore processed exactly
+ * once, by oracle_one(), and the result is identical to the serial loop
+ * because integer addition is associative and commutative.         */
+typedef struct {
+    const uint64_t* ts; const uint32_t* src; const uint32_t* dst; const uint64_t* bytes;
+    uint64_t n; const uint32_t* nets; const uint8_t* lens; uint32_t p;
+    uint64_t start, window; uint32_t width; const uint8_t* lut;
+    uint64_t* out_count; uint64_t* out_bytes;
+    uint64_t slab_lo, slab_hi;   /* bins [slab_lo, slab_hi) */
+    int take_unbinned;
+    uint64_t totals[12];
+} oracle_job;
+
+static void* oracle_worker(void* arg)
+{
+    oracle_job* j = (oracle_job*)arg;
+    uint64_t nbins = j->window / j->width;
+    memset(j->totals, 0, sizeof j->totals);
+    for (uint64_t r = 0; r < j->n; ++r) {
+        uint64_t ts = j->ts[r];
+        int in_window = !(ts < j->start || ts - j->start >= j->window);
+        if (in_window) {
+            uint64_t key = (ts - j->start) / (uint64_t)j->width;
+            if (key < j->slab_lo || key >= j->slab_hi) continue;
+            /* binned or NEITHER-in-window: this slab's thread owns it */
+        } else if (!j->take_unbinned) {
+            continue;
+        }
+        oracle_one(ts, j->src[r], j->dst[r], j->bytes[r], j->nets, j->lens, j->p,
+                   j->start, j->window, j->width, j->lut, nbins,
+                   j->out_count, j->out_bytes, j->totals);
+    }
+    return NULL;
+}
+
+int oracle_classify_histogram_mt(const uint64_t* ts, const uint32_t* src, const uint32_t* dst,
+                                 const uint64_t* bytes, uint64_t n,
+                                 const uint32_t* nets, const uint8_t* lens, uint32_t p,
+                                 uint64_t start, uint64_t window, uint32_t width,
+                                 const uint8_t lut[4],
+                                 uint64_t* out_count, uint64_t* out_bytes, uint64_t* totals,
+                                 int threads)
+{
+    if (threads < 1) threads = 1;
+    uint64_t nbins = window / width;
+    oracle_job* jobs = (oracle_job*)calloc((size_t)threads, sizeof(oracle_job));
+    pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    if (!jobs || !tid) { free(jobs); free(tid); return -1; }
+    for (int t = 0; t < threads; ++t) {
+        oracle_job* j = &jobs[t];
+        j->ts = ts; j->src = src; j->dst = dst; j->bytes = bytes; j->n = n;
+        j->nets = nets; j->lens = lens; j->p = p;
+        j->start = start; j->window = window; j->width = width; j->lut = lut;
+        j->out_count = out_count; j->out_bytes = out_bytes;
+        j->slab_lo = nbins * (uint64_t)t / (uint64_t)threads;
+        j->slab_hi = nbins * (uint64_t)(t + 1) / (uint64_t)threads;
+        j->take_unbinned = (t == 0);
+    }
+    int rc = 0;
+    for (int t = 1; t < threads; ++t)
+        if (pthread_create(&tid[t], NULL, oracle_worker, &jobs[t]) != 0) { rc = -1; threads = t; break; }
+    oracle_worker(&jobs[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+    if (rc == 0)
+        for (int t = 0; t < threads; ++t)
+            for (int k = 0; k < 12; ++k) totals[k] += jobs[t].totals[k];
+    free(jobs); free(tid);
+    return rc;
+}
