@@ -1,0 +1,221 @@
+/*
+ * sinet.h -- C ABI of the B200-native SINET session discrimination + millisecond
+ * histogram library (libsinet.so), after arXiv 2106.12863.
+ *
+ * What the library computes (the paper's two procedures):
+ *   "Discrimination is dividing session data into ingoing/outgoing with subnet
+ *    mask calculation and network address matching.  Histogramming is grouping
+ *    ingoing/outgoing session data into bins with map-reduce."
+ * For every session record r (Table 1 fields capture_time, source_ip,
+ * destination_ip, bytes):
+ *   s_in = OR over CIDR entries (Y/Z): bitmask(r.src, Z) - bitmask(Y, Z) == 0
+ *   d_in = the same for r.dst                              (Alg. 1 l.4-9)
+ *   dir  = dir_lut[s_in*2 + d_in]  (OUT / IN / NEITHER; readings A1, A2)
+ *   bin  = (r.ts - window_start) / bin_width, if window_start <= r.ts < window_start + window
+ *                                                          (Map; 1 ms bins P:L49)
+ *   bins[bin][dir] += (1, r.bytes)   (mod 2^64)            (Reduce)
+ * plus side totals (membership matrix, out-of-window), and across GPUs the
+ * merge of partial histograms (merge-scatter) as a reduce-scatter
+ * over bin ranges.
+ *
+ * Conventions
+ *  - Every function returns SINET_OK (0) or a negative SINET_E_* code; a
+ *    detail string is then available from sinet_last_error(ctx).
+ *  - Device memory is owned by the CALLER (records, bins, workspace, tags,
+ *    staging).  The library never allocates device memory.  It keeps no
+ *    pointer to caller host memory after a call returns.
+ *  - Every call enqueues work on cfg.stream (a cudaStream_t passed as void*),
+ *    in call order.  Calls that return host data synchronise that stream.
+ *  - A ctx is not thread-safe; distinct ctxs on distinct devices are independent.
+ *  - Addresses are IPv4 as u32 with the first octet most significant (the
+ *    numeric value, not network byte order in memory).
+ */
+#ifndef SINET_H
+#define SINET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SINET_ABI_VERSION 1
+
+/* error codes */
+#define SINET_OK        0
+#define SINET_E_INVAL  -1   /* invalid argument (see each call) */
+#define SINET_E_ALIGN  -2   /* a device column base is not 16-byte aligned */
+#define SINET_E_RANGE  -3   /* bin range outside [0,B) or outside this rank's owned range after reduce */
+#define SINET_E_CUDA   -4   /* CUDA runtime error (asynchronous errors surface at the next synchronising call) */
+#define SINET_E_NCCL   -5   /* NCCL unavailable or failed */
+#define SINET_E_STATE  -6   /* call not allowed in the current state (e.g. classify after reduce without reset) */
+
+/* directions (values of dir_lut and of the `dir` argument) */
+#define SINET_DIR_OUT      0
+#define SINET_DIR_IN       1
+#define SINET_DIR_NEITHER  2
+
+/* metrics (the paper's <timestamp,count> and <timestamp,bytes>) */
+#define SINET_METRIC_COUNT 0
+#define SINET_METRIC_BYTES 1
+
+/* accumulation strategy */
+#define SINET_ORDER_AUTO      0   /* library probes the input's time locality */
+#define SINET_ORDER_STREAM    1   /* records approximately time ordered: tile-claim, write-once bins */
+#define SINET_ORDER_SHUFFLED  2   /* arbitrary order: prefill bins, then L2 atomics */
+
+typedef struct sinet_ctx sinet_ctx;
+
+/* One batch ("chunk") of session records, columnar.
+ * Device pointers for sinet_classify_histogram (each base 16-byte aligned),
+ * host pointers for sinet_classify_histogram_host.  n may be 0.           */
+typedef struct {
+    const uint64_t* ts_ms;   /* capture_time, epoch milliseconds (Table 1 no. 1) */
+    const uint32_t* src;     /* source_ip (no. 5) */
+    const uint32_t* dst;     /* destination_ip (no. 8) */
+    const uint64_t* bytes;   /* bytes (no. 21) */
+    uint64_t n;
+} sinet_records;
+
+typedef struct {
+    uint64_t window_start_ms;  /* first millisecond of the window (reading A13: explicit, no tz logic) */
+    uint64_t window_ms;        /* W; 86,400,000 for one day; 1 <= W < 2^32 */
+    uint32_t bin_width_ms;     /* w >= 1, W % w == 0; B = W / w bins per direction */
+    uint8_t  dir_lut[4];       /* [s_in*2+d_in] -> SINET_DIR_*; presets below */
+    int32_t  device;           /* CUDA device ordinal the ctx lives on */
+    int32_t  rank;             /* this process's rank in [0, world) */
+    int32_t  world;            /* number of ranks (GPUs) sharing one histogram, >= 1 */
+    void*    stream;           /* cudaStream_t all work is enqueued on (NULL = legacy default) */
+    uint32_t order_hint;       /* SINET_ORDER_* */
+    uint32_t reserved[7];      /* must be zero */
+} sinet_config;
+
+/* direction-LUT presets (A1/A2) */
+#define SINET_LUT_SRC_PRIORITY {SINET_DIR_NEITHER, SINET_DIR_IN, SINET_DIR_OUT, SINET_DIR_OUT}
+#define SINET_LUT_ALG1         {SINET_DIR_IN, SINET_DIR_IN, SINET_DIR_OUT, SINET_DIR_OUT}
+#define SINET_LUT_STRICT       {SINET_DIR_NEITHER, SINET_DIR_IN, SINET_DIR_OUT, SINET_DIR_NEITHER}
+
+/* Side totals, all u64 modulo 2^64. */
+typedef struct {
+    uint64_t m_count[4];   /* membership matrix over every record, index s_in*2+d_in */
+    uint64_t m_bytes[4];
+    uint64_t oow_count[2]; /* per dir OUT/IN: records outside the window (counted, not binned, A14) */
+    uint64_t oow_bytes[2];
+} sinet_totals;
+
+/* ---------------------------------------------------------------- sizing */
+/* Device bytes the bins buffer needs: 32 * B_pad, B_pad = B rounded up to a
+ * multiple of world * SINET_TILE_BINS.  Layout: u64 bins[B_pad][2 dir][2 metric]
+ * (count, bytes) -- one 32-byte DRAM sector per millisecond bin.  0 if cfg invalid. */
+size_t sinet_bins_bytes(const sinet_config* cfg);
+
+/* Device bytes of workspace for a table of n_prefixes entries (compiled
+ * prefix table, per-tile state flags, totals).  0 if cfg invalid. */
+size_t sinet_workspace_bytes(const sinet_config* cfg, uint32_t n_prefixes);
+
+/* Device staging bytes sinet_classify_histogram_host needs to stream host
+ * records in chunks of chunk_records (double buffered). */
+size_t sinet_staging_bytes(uint64_t chunk_records);
+
+/* ---------------------------------------------------------------- lifecycle */
+/* Create a ctx.  Copies and compiles the CIDR list ("CIDR list", Alg. 1 l.1,
+ * P:L155; Y.Y.Y.Y/Z, l.4): host bits of prefix_net are cleared (Alg. 1 l.7,
+ * reading A9), duplicates dropped, the union compiled to a lookup table in the
+ * workspace.  The histogram starts empty (all bins and totals zero).
+ * d_bins / d_ws: device buffers of at least sinet_bins_bytes / sinet_workspace_bytes,
+ * 256-byte aligned.  Synchronises cfg.stream before returning.
+ * Errors: E_INVAL (n_prefixes == 0, a prefix_len > 32, bin_width 0, W % w != 0,
+ * W == 0 or W >= 2^32, window_start + W overflows, world < 1, rank outside
+ * [0,world), dir_lut entry > 2, reserved != 0, buffer too small or misaligned),
+ * E_CUDA. */
+int sinet_open(sinet_ctx** out, const sinet_config* cfg,
+               const uint32_t* prefix_net, const uint8_t* prefix_len, uint32_t n_prefixes,
+               void* d_bins, size_t bins_bytes, void* d_ws, size_t ws_bytes);
+
+/* Destroy a ctx (does not free caller memory).  NULL is a no-op. */
+void sinet_close(sinet_ctx* ctx);
+
+/* Start a new, empty histogram (all bins and totals zero) without touching
+ * the bins buffer (O(1): bins become "virtually zero" by epoch, DESIGN.md
+ * "Tile states").  Clears the reduced state. */
+int sinet_reset(sinet_ctx* ctx);
+
+/* ---------------------------------------------------------------- the hot path */
+/* Discriminate every record of `recs` (device pointers) and ACCUMULATE its
+ * count and bytes into its (bin, dir).  Calling it on k batches
+ * equals calling it once on their concatenation (work queue chunks).
+ * d_tags (nullable, device, n bytes): per-record tag s_in | d_in<<1 | oow<<2.
+ * Errors: E_INVAL (NULL column with n > 0), E_ALIGN, E_STATE (after reduce
+ * without reset), E_CUDA (launch failure). */
+int sinet_classify_histogram(sinet_ctx* ctx, const sinet_records* recs, uint8_t* d_tags);
+
+/* The same, with HOST record columns: the library streams them through the
+ * caller's device staging buffer (sinet_staging_bytes(chunk_records) bytes)
+ * in chunks, overlapping host->device copies with the kernel.  Pinned host
+ * memory makes the copies asynchronous.  Synchronises cfg.stream. */
+int sinet_classify_histogram_host(sinet_ctx* ctx, const sinet_records* host_recs,
+                                  void* d_staging, size_t staging_bytes, uint64_t chunk_records);
+
+/* Materialise every bin (zero-fill tiles no record touched).  Idempotent;
+ * called implicitly by sinet_reduce and sinet_read_bins. */
+int sinet_finalize(sinet_ctx* ctx);
+
+/* ---------------------------------------------------------------- multi-GPU */
+/* Build this rank's NCCL communicator from a 128-byte ncclUniqueId created by
+ * rank 0 and shared by the caller (e.g. through torch.distributed).  NCCL is
+ * loaded at run time (the libnccl.so.2 already in the process, else by name).
+ * Errors: E_NCCL, E_INVAL (world == 1 needs no comm). */
+int sinet_comm_init(sinet_ctx* ctx, const void* nccl_unique_id);
+
+/* Create a fresh 128-byte ncclUniqueId (rank 0), to be shared with the other
+ * ranks before sinet_comm_init.  Errors: E_NCCL, E_INVAL (NULL out). */
+int sinet_nccl_unique_id(void* out128);
+
+/* Merge the per-GPU partial histograms (merge-scatter): finalize,
+ * then an in-place reduce-scatter (u64 sum) leaves rank g the global sums of
+ * bins [g*B_pad/world, (g+1)*B_pad/world); totals are all-reduced so every
+ * rank holds the global totals.  world == 1: finalize only.
+ * Errors: E_STATE (already reduced), E_NCCL (no comm / NCCL failure). */
+int sinet_reduce(sinet_ctx* ctx);
+
+/* Owned bin range: [0, B) before reduce or with world == 1, else this rank's
+ * slice clipped to [0, B). */
+int sinet_owned_range(sinet_ctx* ctx, uint64_t* first_bin, uint64_t* n_bins);
+
+/* ---------------------------------------------------------------- read-out */
+/* Copy bins [first_bin, first_bin + n_bins) of one (dir, metric) plane into
+ * dst (u64[n_bins]; device if dst_is_device else host, host copies
+ * synchronise the stream).  Errors: E_INVAL (dir not OUT/IN, metric not
+ * COUNT/BYTES, NULL dst), E_RANGE (outside the owned range), E_CUDA. */
+int sinet_read_bins(sinet_ctx* ctx, int dir, int metric, uint64_t first_bin, uint64_t n_bins,
+                    uint64_t* dst, int dst_is_device);
+
+/* Copy the totals to host (synchronises the stream). */
+int sinet_read_totals(sinet_ctx* ctx, sinet_totals* out);
+
+/* ---------------------------------------------------------------- introspection */
+const char* sinet_last_error(const sinet_ctx* ctx);
+/* Number of kernels this ctx has launched since open (all kinds). */
+uint64_t sinet_launch_count(const sinet_ctx* ctx);
+/* Enable (1) / disable (0) CUDA-event timing of the main classify kernel on
+ * cfg.stream; sinet_kernel_time reads back the summed duration (ms) and the
+ * number of timed launches since enabling (synchronises the stream). */
+int sinet_set_kernel_timing(sinet_ctx* ctx, int on);
+int sinet_kernel_time(sinet_ctx* ctx, double* total_ms, uint64_t* launches);
+/* Which accumulation strategy the last classify call used (SINET_ORDER_STREAM/SHUFFLED). */
+int sinet_last_strategy(const sinet_ctx* ctx);
+/* Host-side check of the prefix compiler (no GPU needed): compiles the CIDR
+ * list exactly as sinet_open does and evaluates the same /16-class + boundary
+ * lookup the kernels use, on the host, for ips[0..n): out[i] = member (0/1).
+ * Errors: E_INVAL as sinet_open's table checks. */
+int sinet_table_member_host(const uint32_t* prefix_net, const uint8_t* prefix_len, uint32_t n_prefixes,
+                            const uint32_t* ips, uint64_t n, uint8_t* out);
+/* Compile-time constants of this build. */
+uint32_t sinet_tile_bins(void);
+int sinet_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINET_H */

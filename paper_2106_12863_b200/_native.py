@@ -1,0 +1,100 @@
+"""ctypes binding of libsinet.so (include/sinet.h).  Argument marshalling only.
+
+The product path has no CPU fallback: if the CUDA library is missing this
+module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsinet.so")
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "sinet.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libsinet.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+OK, E_INVAL, E_ALIGN, E_RANGE, E_CUDA, E_NCCL, E_STATE = 0, -1, -2, -3, -4, -5, -6
+ERR_NAMES = {E_INVAL: "E_INVAL", E_ALIGN: "E_ALIGN", E_RANGE: "E_RANGE", E_CUDA: "E_CUDA",
+             E_NCCL: "E_NCCL", E_STATE: "E_STATE"}
+DIR_OUT, DIR_IN, DIR_NEITHER = 0, 1, 2
+METRIC_COUNT, METRIC_BYTES = 0, 1
+ORDER_AUTO, ORDER_STREAM, ORDER_SHUFFLED = 0, 1, 2
+LUT_SRC_PRIORITY = (DIR_NEITHER, DIR_IN, DIR_OUT, DIR_OUT)
+LUT_ALG1 = (DIR_IN, DIR_IN, DIR_OUT, DIR_OUT)
+LUT_STRICT = (DIR_NEITHER, DIR_IN, DIR_OUT, DIR_NEITHER)
+
+
+class Records(ctypes.Structure):
+    _fields_ = [("ts_ms", ctypes.c_void_p), ("src", ctypes.c_void_p), ("dst", ctypes.c_void_p),
+                ("bytes", ctypes.c_void_p), ("n", ctypes.c_uint64)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("window_start_ms", ctypes.c_uint64), ("window_ms", ctypes.c_uint64),
+                ("bin_width_ms", ctypes.c_uint32), ("dir_lut", ctypes.c_uint8 * 4),
+                ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("order_hint", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 7)]
+
+
+class Totals(ctypes.Structure):
+    _fields_ = [("m_count", ctypes.c_uint64 * 4), ("m_bytes", ctypes.c_uint64 * 4),
+                ("oow_count", ctypes.c_uint64 * 2), ("oow_bytes", ctypes.c_uint64 * 2)]
+
+
+_vp, _u64, _u32, _i = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+_CP = ctypes.POINTER(Config)
+_SIGS = {
+    "sinet_abi_version": ([], _i),
+    "sinet_tile_bins": ([], _u32),
+    "sinet_bins_bytes": ([_CP], ctypes.c_size_t),
+    "sinet_workspace_bytes": ([_CP, _u32], ctypes.c_size_t),
+    "sinet_staging_bytes": ([_u64], ctypes.c_size_t),
+    "sinet_open": ([ctypes.POINTER(_vp), _CP, _vp, _vp, _u32, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t], _i),
+    "sinet_close": ([_vp], None),
+    "sinet_reset": ([_vp], _i),
+    "sinet_classify_histogram": ([_vp, ctypes.POINTER(Records), _vp], _i),
+    "sinet_classify_histogram_host": ([_vp, ctypes.POINTER(Records), _vp, ctypes.c_size_t, _u64], _i),
+    "sinet_finalize": ([_vp], _i),
+    "sinet_comm_init": ([_vp, _vp], _i),
+    "sinet_nccl_unique_id": ([_vp], _i),
+    "sinet_reduce": ([_vp], _i),
+    "sinet_owned_range": ([_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i),
+    "sinet_read_bins": ([_vp, _i, _i, _u64, _u64, _vp, _i], _i),
+    "sinet_read_totals": ([_vp, ctypes.POINTER(Totals)], _i),
+    "sinet_last_error": ([_vp], ctypes.c_char_p),
+    "sinet_launch_count": ([_vp], _u64),
+    "sinet_set_kernel_timing": ([_vp, _i], _i),
+    "sinet_kernel_time": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)], _i),
+    "sinet_last_strategy": ([_vp], _i),
+    "sinet_table_member_host": ([_vp, _vp, _u32, _vp, _u64, _vp], _i),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def header_functions():
+    """Names of every function declared in include/sinet.h."""
+    with open(HEADER) as f:
+        txt = re.sub(r"/\*.*?\*/", "", f.read(), flags=re.S)
+    return sorted(set(re.findall(r"\b(sinet_[a-z0-9_]+)\s*\(", txt)))
+
+
+class SinetError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def check(rc, ctx=None, what=""):
+    if rc != OK:
+        msg = lib.sinet_last_error(ctx).decode() if ctx else ""
+        raise SinetError(rc, f"{what}: {msg}" if what else msg)
+    return rc

@@ -1,0 +1,35 @@
+// Host-side compilation of the CIDR list into the device lookup table.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sinet {
+
+// Device lookup table for membership of a u32 address in the union of the
+// CIDR entries (Alg. 1 l.4-9).
+//
+//   bnd[K]     sorted, distinct u32 boundaries of the merged member intervals:
+//              every interval [lo, hi] contributes lo and (if hi < 2^32-1) hi+1.
+//              member(ip) == (number of boundaries <= ip) is odd.
+//   cls2[4096] 2-bit class per /16 block x = ip >> 16, 16 per word:
+//              0 = no address of the block is a member, 1 = all are, 2 = mixed.
+//   entry[65536] for block x: lo | len << 16, where lo = #boundaries <= x<<16
+//              and len = #boundaries in (x<<16, x<<16 | 0xFFFF]; a mixed block's
+//              member(ip) = (lo + #{bnd[lo..lo+len) <= ip}) & 1.
+struct CompiledTable {
+    std::vector<uint32_t> bnd;
+    std::vector<uint32_t> cls2;
+    std::vector<uint32_t> entry;
+    uint32_t n_unique = 0;     // distinct normalised entries
+    uint32_t n_intervals = 0;  // merged member intervals
+    uint32_t n_mixed = 0;      // /16 blocks of class 2
+};
+
+constexpr uint32_t kMaxPrefixes = 32767;   // keeps lo and len in 16 bits each
+
+// Returns false (with *err set) on invalid input (n == 0, len > 32, n > kMaxPrefixes).
+bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
+                      CompiledTable* out, std::string* err);
+
+}  // namespace sinet

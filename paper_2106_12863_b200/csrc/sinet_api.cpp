@@ -1,0 +1,547 @@
+// libsinet C ABI (include/sinet.h): context lifecycle, validation, launch
+// planning, NCCL merge and read-out.  All device memory is the caller's.
+#include "sinet.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "prefix_compile.h"
+#include "sinet_kernels.h"
+
+using namespace sinet;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (run-time loaded)
+// Minimal declarations of the NCCL 2.x C API (values from nccl.h 2.28).
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclSum = 0;
+constexpr int kNcclUint64 = 5;
+
+struct NcclApi {
+    bool loaded = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl_api(std::string* err) {
+    static NcclApi api;
+    if (api.loaded) return &api;
+    // prefer the libnccl.so.2 already mapped into the process (torch's), else load by name
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { *err = std::string("cannot load libnccl.so.2: ") + dlerror(); return nullptr; }
+#define SINET_SYM(field, name) \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name)); \
+    if (!api.field) { *err = std::string("libnccl.so.2 lacks ") + name; return nullptr; }
+    SINET_SYM(GetUniqueId, "ncclGetUniqueId")
+    SINET_SYM(CommInitRank, "ncclCommInitRank")
+    SINET_SYM(CommDestroy, "ncclCommDestroy")
+    SINET_SYM(ReduceScatter, "ncclReduceScatter")
+    SINET_SYM(AllReduce, "ncclAllReduce")
+    SINET_SYM(GroupStart, "ncclGroupStart")
+    SINET_SYM(GroupEnd, "ncclGroupEnd")
+    SINET_SYM(GetErrorString, "ncclGetErrorString")
+#undef SINET_SYM
+    api.loaded = true;
+    return &api;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Geometry {
+    uint64_t B = 0, B_pad = 0, n_tiles = 0;
+};
+
+bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
+    if (!c) { *err = "NULL config"; return false; }
+    if (c->window_ms == 0 || c->window_ms >= (1ull << 32)) { *err = "window_ms must be in [1, 2^32)"; return false; }
+    if (c->bin_width_ms == 0) { *err = "bin_width_ms must be >= 1"; return false; }
+    if (c->window_ms % c->bin_width_ms != 0) { *err = "window_ms must be a multiple of bin_width_ms"; return false; }
+    if (c->window_start_ms > ~0ull - c->window_ms) { *err = "window_start_ms + window_ms overflows u64"; return false; }
+    if (c->world < 1 || c->world > 4096) { *err = "world must be in [1, 4096]"; return false; }
+    if (c->rank < 0 || c->rank >= c->world) { *err = "rank must be in [0, world)"; return false; }
+    for (int k = 0; k < 4; ++k)
+        if (c->dir_lut[k] > SINET_DIR_NEITHER) { *err = "dir_lut entries must be 0 (OUT), 1 (IN) or 2 (NEITHER)"; return false; }
+    if (c->order_hint > SINET_ORDER_SHUFFLED) { *err = "order_hint must be SINET_ORDER_*"; return false; }
+    for (int k = 0; k < 7; ++k)
+        if (c->reserved[k]) { *err = "reserved fields must be zero"; return false; }
+    g->B = c->window_ms / c->bin_width_ms;
+    uint64_t unit = (uint64_t)c->world * kTileBins;
+    g->B_pad = (g->B + unit - 1) / unit * unit;
+    g->n_tiles = g->B_pad / kTileBins;
+    return true;
+}
+
+struct WsLayout {
+    size_t totals, cls2, entry, bnd, flags, total;
+};
+
+WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
+    WsLayout L{};
+    size_t off = 0;
+    L.totals = off; off = align_up(off + 16 * 8, 256);
+    L.cls2 = off;   off = align_up(off + (size_t)kClsWords * 4, 256);
+    L.entry = off;  off = align_up(off + 65536 * 4, 256);
+    L.bnd = off;    off = align_up(off + ((size_t)2 * n_prefixes + 1) * 4, 256);
+    L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
+    L.total = off;
+    return L;
+}
+
+}  // namespace
+
+struct sinet_ctx {
+    sinet_config cfg{};
+    Geometry geo;
+    WsLayout ws{};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    int sm_count = 0;
+    int atomic_grid = 0;
+    int materialize_grid = 0;
+    unsigned long long* bins = nullptr;
+    unsigned char* d_ws = nullptr;
+    uint32_t nbnd = 0;
+    uint32_t lut = 0;
+    uint32_t magic = 0;
+    uint32_t epoch = 1;
+    bool reduced = false;
+    bool materialized = false;
+    int last_strategy = 0;
+    uint64_t launches = 0;
+    ncclComm_t comm = nullptr;
+    // host-streaming pipeline
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_done[2] = {nullptr, nullptr};
+    cudaEvent_t kern_done[2] = {nullptr, nullptr};
+    // optional kernel timing
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    std::string err;
+    CompiledTable table;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int fail(sinet_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(sinet_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, SINET_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define SINET_CUDA(ctx, expr)                                    \
+    do {                                                         \
+        cudaError_t e_ = (expr);                                 \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr); \
+    } while (0)
+
+uint32_t* ws_u32(sinet_ctx* c, size_t off) { return reinterpret_cast<uint32_t*>(c->d_ws + off); }
+
+KernelParams base_params(sinet_ctx* c) {
+    KernelParams p{};
+    p.bins = c->bins;
+    p.totals = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.totals);
+    p.tile_flags = ws_u32(c, c->ws.flags);
+    p.cls2 = ws_u32(c, c->ws.cls2);
+    p.entry = ws_u32(c, c->ws.entry);
+    p.bnd = ws_u32(c, c->ws.bnd);
+    p.nbnd = c->nbnd;
+    p.lut = c->lut;
+    p.start = c->cfg.window_start_ms;
+    p.window = (uint32_t)c->cfg.window_ms;
+    p.width = c->cfg.bin_width_ms;
+    p.magic = c->magic;
+    p.nbins = (uint32_t)c->geo.B;
+    p.epoch = c->epoch;
+    p.n_tiles = (uint32_t)c->geo.n_tiles;
+    return p;
+}
+
+uint32_t init_word(const sinet_ctx* c) { return (c->epoch << 2) | kTileInit; }
+
+int do_materialize(sinet_ctx* c) {
+    if (c->materialized) return SINET_OK;
+    SINET_CUDA(c, launch_materialize(c->bins, ws_u32(c, c->ws.flags), (uint32_t)c->geo.n_tiles,
+                                     init_word(c), c->materialize_grid, c->stream));
+    c->launches++;
+    c->materialized = true;
+    return SINET_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
+    if (c->reduced) return fail(c, SINET_E_STATE, "classify after reduce: call sinet_reset first");
+    if (!r) return fail(c, SINET_E_INVAL, "NULL records");
+    if (r->n == 0) return SINET_OK;
+    if (!r->ts_ms || !r->src || !r->dst || !r->bytes) return fail(c, SINET_E_INVAL, "NULL record column");
+    if (!aligned16(r->ts_ms) || !aligned16(r->src) || !aligned16(r->dst) || !aligned16(r->bytes))
+        return fail(c, SINET_E_ALIGN, "record columns must be 16-byte aligned");
+    if (d_tags && (reinterpret_cast<uintptr_t>(d_tags) & 3u))
+        return fail(c, SINET_E_ALIGN, "tags buffer must be 4-byte aligned");
+    KernelParams p = base_params(c);
+    p.ts = r->ts_ms; p.src = r->src; p.dst = r->dst; p.bytes = r->bytes; p.n = r->n; p.tags = d_tags;
+
+    // strategy SHUFFLED (v0): materialise every tile, then L2 atomics
+    int rc = do_materialize(c);
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        SINET_CUDA(c, cudaEventCreate(&e0));
+        SINET_CUDA(c, cudaEventCreate(&e1));
+        SINET_CUDA(c, cudaEventRecord(e0, c->stream));
+    }
+    SINET_CUDA(c, launch_hist_atomic(p, c->atomic_grid, c->stream));
+    c->launches++;
+    c->last_strategy = SINET_ORDER_SHUFFLED;
+    if (c->timing) {
+        SINET_CUDA(c, cudaEventRecord(e1, c->stream));
+        c->tev.emplace_back(e0, e1);
+    }
+    // bins stay materialised: atomics only add to initialised tiles
+    return SINET_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sinet_abi_version(void) { return SINET_ABI_VERSION; }
+uint32_t sinet_tile_bins(void) { return kTileBins; }
+
+size_t sinet_bins_bytes(const sinet_config* cfg) {
+    std::string err;
+    Geometry g;
+    if (!check_cfg(cfg, &err, &g)) return 0;
+    return (size_t)g.B_pad * 32u;
+}
+
+size_t sinet_workspace_bytes(const sinet_config* cfg, uint32_t n_prefixes) {
+    std::string err;
+    Geometry g;
+    if (!check_cfg(cfg, &err, &g) || n_prefixes == 0 || n_prefixes > kMaxPrefixes) return 0;
+    return ws_layout(g.n_tiles, n_prefixes).total;
+}
+
+size_t sinet_staging_bytes(uint64_t chunk_records) {
+    if (chunk_records == 0) return 0;
+    size_t per = align_up(chunk_records * 8, 256) * 2 + align_up(chunk_records * 4, 256) * 2;
+    return per * 2;
+}
+
+int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_net,
+               const uint8_t* prefix_len, uint32_t n_prefixes, void* d_bins, size_t bins_bytes,
+               void* d_ws, size_t ws_bytes) {
+    if (!out) return SINET_E_INVAL;
+    *out = nullptr;
+    sinet_ctx* c = new (std::nothrow) sinet_ctx();
+    if (!c) return SINET_E_INVAL;
+    auto bail = [&](int code) { delete c; return code; };
+    Geometry g;
+    if (!check_cfg(cfg, &c->err, &g)) { std::fprintf(stderr, "sinet_open: %s\n", c->err.c_str()); return bail(SINET_E_INVAL); }
+    if (!compile_prefixes(prefix_net, prefix_len, n_prefixes, &c->table, &c->err)) {
+        std::fprintf(stderr, "sinet_open: %s\n", c->err.c_str());
+        return bail(SINET_E_INVAL);
+    }
+    c->cfg = *cfg;
+    c->geo = g;
+    c->ws = ws_layout(g.n_tiles, n_prefixes);
+    if (!d_bins || !d_ws || bins_bytes < (size_t)g.B_pad * 32u || ws_bytes < c->ws.total ||
+        (reinterpret_cast<uintptr_t>(d_bins) & 255u) || (reinterpret_cast<uintptr_t>(d_ws) & 255u)) {
+        std::fprintf(stderr, "sinet_open: bins/workspace buffer missing, too small or not 256-byte aligned\n");
+        return bail(SINET_E_INVAL);
+    }
+    c->bins = static_cast<unsigned long long*>(d_bins);
+    c->d_ws = static_cast<unsigned char*>(d_ws);
+    c->stream = static_cast<cudaStream_t>(cfg->stream);
+    c->device = cfg->device;
+    c->nbnd = (uint32_t)c->table.bnd.size();
+    for (int k = 0; k < 4; ++k) c->lut |= (uint32_t)cfg->dir_lut[k] << (2 * k);
+    c->magic = (cfg->bin_width_ms >= 2) ? (uint32_t)((1ull << 32) / cfg->bin_width_ms) : 0u;
+
+    DeviceGuard dg(c->device);
+    if (!dg.ok) { std::fprintf(stderr, "sinet_open: cannot select device %d\n", c->device); return bail(SINET_E_CUDA); }
+    cudaError_t e;
+#define OPEN_CUDA(expr) \
+    if ((e = (expr)) != cudaSuccess) { std::fprintf(stderr, "sinet_open: %s: %s\n", #expr, cudaGetErrorString(e)); return bail(SINET_E_CUDA); }
+    OPEN_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+    OPEN_CUDA(setup_hist_atomic());
+    c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(c->nbnd);
+    c->materialize_grid = c->sm_count * 8;
+    // upload the compiled table; zero totals and tile states
+    OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.totals, 0, 16 * 8, c->stream));
+    OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.cls2, c->table.cls2.data(), (size_t)kClsWords * 4, cudaMemcpyHostToDevice, c->stream));
+    OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.entry, c->table.entry.data(), 65536 * 4, cudaMemcpyHostToDevice, c->stream));
+    if (c->nbnd)
+        OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.bnd, c->table.bnd.data(), (size_t)c->nbnd * 4, cudaMemcpyHostToDevice, c->stream));
+    OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
+    OPEN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        OPEN_CUDA(cudaEventCreateWithFlags(&c->copy_done[k], cudaEventDisableTiming));
+        OPEN_CUDA(cudaEventCreateWithFlags(&c->kern_done[k], cudaEventDisableTiming));
+    }
+    OPEN_CUDA(cudaStreamSynchronize(c->stream));
+#undef OPEN_CUDA
+    *out = c;
+    return SINET_OK;
+}
+
+void sinet_close(sinet_ctx* c) {
+    if (!c) return;
+    {
+        DeviceGuard dg(c->device);
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        for (auto& pr : c->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+        for (int k = 0; k < 2; ++k) {
+            if (c->copy_done[k]) cudaEventDestroy(c->copy_done[k]);
+            if (c->kern_done[k]) cudaEventDestroy(c->kern_done[k]);
+        }
+        if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+        if (c->comm) {
+            std::string err;
+            NcclApi* api = nccl_api(&err);
+            if (api) api->CommDestroy(c->comm);
+        }
+    }
+    delete c;
+}
+
+int sinet_reset(sinet_ctx* c) {
+    if (!c) return SINET_E_INVAL;
+    DeviceGuard dg(c->device);
+    SINET_CUDA(c, cudaMemsetAsync(c->d_ws + c->ws.totals, 0, 16 * 8, c->stream));
+    c->epoch++;
+    if (c->epoch >= (1u << 30)) {   // epoch space exhausted: re-zero the state words
+        SINET_CUDA(c, cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)c->geo.n_tiles * 4, c->stream));
+        c->epoch = 1;
+    }
+    c->reduced = false;
+    c->materialized = false;
+    return SINET_OK;
+}
+
+int sinet_classify_histogram(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
+    if (!c) return SINET_E_INVAL;
+    DeviceGuard dg(c->device);
+    return classify_device(c, r, d_tags);
+}
+
+int sinet_classify_histogram_host(sinet_ctx* c, const sinet_records* h, void* d_staging,
+                                  size_t staging_bytes, uint64_t chunk) {
+    if (!c) return SINET_E_INVAL;
+    if (!h) return fail(c, SINET_E_INVAL, "NULL records");
+    if (c->reduced) return fail(c, SINET_E_STATE, "classify after reduce: call sinet_reset first");
+    if (h->n == 0) return SINET_OK;
+    if (!h->ts_ms || !h->src || !h->dst || !h->bytes) return fail(c, SINET_E_INVAL, "NULL record column");
+    if (chunk == 0 || !d_staging || staging_bytes < sinet_staging_bytes(chunk) ||
+        (reinterpret_cast<uintptr_t>(d_staging) & 255u))
+        return fail(c, SINET_E_INVAL, "staging buffer missing, too small or not 256-byte aligned");
+    DeviceGuard dg(c->device);
+    const size_t o_ts = 0, o_src = align_up(chunk * 8, 256), o_dst = o_src + align_up(chunk * 4, 256),
+                 o_by = o_dst + align_up(chunk * 4, 256), per = o_by + align_up(chunk * 8, 256);
+    unsigned char* stage = static_cast<unsigned char*>(d_staging);
+    uint64_t k = 0;
+    for (uint64_t lo = 0; lo < h->n; lo += chunk, ++k) {
+        const uint64_t m = (h->n - lo < chunk) ? h->n - lo : chunk;
+        const int b = (int)(k & 1);
+        unsigned char* buf = stage + per * b;
+        if (k >= 2) SINET_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->kern_done[b], 0));
+        SINET_CUDA(c, cudaMemcpyAsync(buf + o_ts, h->ts_ms + lo, m * 8, cudaMemcpyHostToDevice, c->copy_stream));
+        SINET_CUDA(c, cudaMemcpyAsync(buf + o_src, h->src + lo, m * 4, cudaMemcpyHostToDevice, c->copy_stream));
+        SINET_CUDA(c, cudaMemcpyAsync(buf + o_dst, h->dst + lo, m * 4, cudaMemcpyHostToDevice, c->copy_stream));
+        SINET_CUDA(c, cudaMemcpyAsync(buf + o_by, h->bytes + lo, m * 8, cudaMemcpyHostToDevice, c->copy_stream));
+        SINET_CUDA(c, cudaEventRecord(c->copy_done[b], c->copy_stream));
+        SINET_CUDA(c, cudaStreamWaitEvent(c->stream, c->copy_done[b], 0));
+        sinet_records dr{reinterpret_cast<const uint64_t*>(buf + o_ts), reinterpret_cast<const uint32_t*>(buf + o_src),
+                         reinterpret_cast<const uint32_t*>(buf + o_dst), reinterpret_cast<const uint64_t*>(buf + o_by), m};
+        int rc = classify_device(c, &dr, nullptr);
+        if (rc) return rc;
+        SINET_CUDA(c, cudaEventRecord(c->kern_done[b], c->stream));
+    }
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SINET_OK;
+}
+
+int sinet_finalize(sinet_ctx* c) {
+    if (!c) return SINET_E_INVAL;
+    if (c->reduced) return SINET_OK;
+    DeviceGuard dg(c->device);
+    return do_materialize(c);
+}
+
+int sinet_nccl_unique_id(void* out) {
+    if (!out) return SINET_E_INVAL;
+    std::string err;
+    NcclApi* api = nccl_api(&err);
+    if (!api) { std::fprintf(stderr, "sinet_nccl_unique_id: %s\n", err.c_str()); return SINET_E_NCCL; }
+    ncclUniqueId id;
+    if (api->GetUniqueId(&id) != 0) return SINET_E_NCCL;
+    std::memcpy(out, &id, sizeof id);
+    return SINET_OK;
+}
+
+int sinet_comm_init(sinet_ctx* c, const void* uid) {
+    if (!c) return SINET_E_INVAL;
+    if (c->cfg.world == 1) return fail(c, SINET_E_INVAL, "world == 1 needs no communicator");
+    if (!uid) return fail(c, SINET_E_INVAL, "NULL unique id");
+    if (c->comm) return fail(c, SINET_E_STATE, "communicator already initialised");
+    NcclApi* api = nccl_api(&c->err);
+    if (!api) return SINET_E_NCCL;
+    DeviceGuard dg(c->device);
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    ncclResult_t r = api->CommInitRank(&c->comm, c->cfg.world, id, c->cfg.rank);
+    if (r != 0) { c->comm = nullptr; return fail(c, SINET_E_NCCL, std::string("ncclCommInitRank: ") + api->GetErrorString(r)); }
+    return SINET_OK;
+}
+
+int sinet_reduce(sinet_ctx* c) {
+    if (!c) return SINET_E_INVAL;
+    if (c->reduced) return fail(c, SINET_E_STATE, "already reduced: call sinet_reset first");
+    DeviceGuard dg(c->device);
+    int rc = do_materialize(c);
+    if (rc) return rc;
+    if (c->cfg.world > 1) {
+        if (!c->comm) return fail(c, SINET_E_NCCL, "no communicator: call sinet_comm_init");
+        NcclApi* api = nccl_api(&c->err);
+        if (!api) return SINET_E_NCCL;
+        const size_t slice = (size_t)(c->geo.B_pad / (uint64_t)c->cfg.world) * 4u;   // u64 per rank
+        unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.totals);
+        ncclResult_t r = api->GroupStart();
+        if (r == 0) r = api->ReduceScatter(c->bins, c->bins + slice * (size_t)c->cfg.rank, slice,
+                                           kNcclUint64, kNcclSum, c->comm, c->stream);
+        if (r == 0) r = api->AllReduce(tot, tot, 12, kNcclUint64, kNcclSum, c->comm, c->stream);
+        ncclResult_t r2 = api->GroupEnd();
+        if (r == 0) r = r2;
+        if (r != 0) return fail(c, SINET_E_NCCL, std::string("NCCL reduce: ") + api->GetErrorString(r));
+    }
+    c->reduced = true;
+    return SINET_OK;
+}
+
+int sinet_owned_range(sinet_ctx* c, uint64_t* first, uint64_t* n) {
+    if (!c || !first || !n) return SINET_E_INVAL;
+    if (!c->reduced || c->cfg.world == 1) { *first = 0; *n = c->geo.B; return SINET_OK; }
+    uint64_t per = c->geo.B_pad / (uint64_t)c->cfg.world;
+    uint64_t lo = per * (uint64_t)c->cfg.rank, hi = lo + per;
+    if (lo > c->geo.B) lo = c->geo.B;
+    if (hi > c->geo.B) hi = c->geo.B;
+    *first = lo;
+    *n = hi - lo;
+    return SINET_OK;
+}
+
+int sinet_read_bins(sinet_ctx* c, int dir, int metric, uint64_t first, uint64_t n, uint64_t* dst, int dst_is_device) {
+    if (!c) return SINET_E_INVAL;
+    if (dir != SINET_DIR_OUT && dir != SINET_DIR_IN) return fail(c, SINET_E_INVAL, "dir must be SINET_DIR_OUT or SINET_DIR_IN");
+    if (metric != SINET_METRIC_COUNT && metric != SINET_METRIC_BYTES) return fail(c, SINET_E_INVAL, "metric must be COUNT or BYTES");
+    uint64_t lo, cnt;
+    sinet_owned_range(c, &lo, &cnt);
+    if (first < lo || first > lo + cnt || n > lo + cnt - first) return fail(c, SINET_E_RANGE, "bin range outside the owned range");
+    if (n == 0) return SINET_OK;
+    if (!dst) return fail(c, SINET_E_INVAL, "NULL destination");
+    DeviceGuard dg(c->device);
+    int rc = c->reduced ? SINET_OK : do_materialize(c);
+    if (rc) return rc;
+    const unsigned long long* srcp = c->bins + (first * 4u + (uint64_t)dir * 2u + (uint64_t)metric);
+    SINET_CUDA(c, cudaMemcpy2DAsync(dst, 8, srcp, 32, 8, n, dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    if (!dst_is_device) SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SINET_OK;
+}
+
+int sinet_read_totals(sinet_ctx* c, sinet_totals* out) {
+    if (!c || !out) return c ? fail(c, SINET_E_INVAL, "NULL output") : SINET_E_INVAL;
+    DeviceGuard dg(c->device);
+    unsigned long long h[12];
+    SINET_CUDA(c, cudaMemcpyAsync(h, c->d_ws + c->ws.totals, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < 4; ++k) { out->m_count[k] = h[k]; out->m_bytes[k] = h[4 + k]; }
+    out->oow_count[0] = h[8]; out->oow_count[1] = h[9];
+    out->oow_bytes[0] = h[10]; out->oow_bytes[1] = h[11];
+    return SINET_OK;
+}
+
+int sinet_table_member_host(const uint32_t* net, const uint8_t* len, uint32_t np,
+                            const uint32_t* ips, uint64_t n, uint8_t* out) {
+    CompiledTable t;
+    std::string err;
+    if (!compile_prefixes(net, len, np, &t, &err)) return SINET_E_INVAL;
+    if (n && (!ips || !out)) return SINET_E_INVAL;
+    for (uint64_t i = 0; i < n; ++i) {
+        // the kernels' lookup (sinet_device.cuh member()), evaluated on the host
+        uint32_t ip = ips[i], x = ip >> 16;
+        uint32_t c = (t.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
+        if (c < 2u) { out[i] = (uint8_t)c; continue; }
+        uint32_t e = t.entry[x], cnt = e & 0xFFFFu, m = e >> 16;
+        const uint32_t* b = t.bnd.data() + cnt;
+        while (m) {
+            uint32_t half = m >> 1;
+            if (b[half] <= ip) { b += half + 1; cnt += half + 1; m -= half + 1; }
+            else m = half;
+        }
+        out[i] = (uint8_t)(cnt & 1u);
+    }
+    return SINET_OK;
+}
+
+const char* sinet_last_error(const sinet_ctx* c) { return c ? c->err.c_str() : "NULL ctx"; }
+uint64_t sinet_launch_count(const sinet_ctx* c) { return c ? c->launches : 0; }
+int sinet_last_strategy(const sinet_ctx* c) { return c ? c->last_strategy : 0; }
+
+int sinet_set_kernel_timing(sinet_ctx* c, int on) {
+    if (!c) return SINET_E_INVAL;
+    DeviceGuard dg(c->device);
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (auto& pr : c->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    c->tev.clear();
+    c->timing = on != 0;
+    return SINET_OK;
+}
+
+int sinet_kernel_time(sinet_ctx* c, double* total_ms, uint64_t* launches) {
+    if (!c || !total_ms || !launches) return SINET_E_INVAL;
+    DeviceGuard dg(c->device);
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    double t = 0;
+    for (auto& pr : c->tev) {
+        float ms = 0;
+        SINET_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
+        t += ms;
+    }
+    *total_ms = t;
+    *launches = c->tev.size();
+    return SINET_OK;
+}
+
+}  // extern "C"

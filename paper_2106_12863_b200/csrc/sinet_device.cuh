@@ -1,0 +1,152 @@
+// Device-side building blocks shared by the sinet kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sinet_params.h"
+
+namespace sinet {
+
+// ---------------------------------------------------------------- a3 + a4: membership
+// Alg. 1 l.6-9 against the compiled union of the CIDR list
+// (prefix_compile.cpp): one shared-memory load decides blocks wholly inside
+// or outside; mixed /16 blocks search their few boundaries.
+__device__ __forceinline__ uint32_t member(uint32_t ip, const uint32_t* s_cls2,
+                                           const uint32_t* __restrict__ entry,
+                                           const uint32_t* bnd) {
+    uint32_t x = ip >> 16;
+    uint32_t c = (s_cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
+    if (c < 2u) return c;
+    uint32_t e = __ldg(entry + x);
+    uint32_t cnt = e & 0xFFFFu, len = e >> 16;
+    const uint32_t* b = bnd + cnt;
+    while (len) {
+        uint32_t half = len >> 1;
+        if (b[half] <= ip) { b += half + 1; cnt += half + 1; len -= half + 1; }
+        else len = half;
+    }
+    return cnt & 1u;
+}
+
+// ---------------------------------------------------------------- a5: Map to a ms bin
+// key = (ts - start) / w for start <= ts < start + W (bins of 1 ms P:L217,
+// half-open, reading A15).  d < W < 2^32, so a 32-bit quotient with one
+// correction step after the multiply-high estimate is exact.
+__device__ __forceinline__ bool map_bin(uint64_t ts, const KernelParams& p, uint32_t& bin) {
+    uint64_t d = ts - p.start;          // wraps for ts < start -> fails the test below
+    if (d >= (uint64_t)p.window) return false;
+    uint32_t d32 = (uint32_t)d;
+    if (p.width == 1u) { bin = d32; return true; }
+    uint32_t q = __umulhi(d32, p.magic);
+    if (d32 - q * p.width >= p.width) ++q;
+    bin = q;
+    return true;
+}
+
+// ---------------------------------------------------------------- a7: side totals
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+    // three exact 32-bit warp reductions of 24/24/16-bit pieces, recombined mod 2^64
+    uint32_t a = __reduce_add_sync(kFull, (uint32_t)(v & 0xFFFFFFu));
+    uint32_t b = __reduce_add_sync(kFull, (uint32_t)((v >> 24) & 0xFFFFFFu));
+    uint32_t c = __reduce_add_sync(kFull, (uint32_t)(v >> 48));
+    return (uint64_t)a + ((uint64_t)b << 24) + ((uint64_t)c << 48);
+}
+
+struct WarpTotals {   // lane-uniform accumulators
+    uint64_t mc[4], mb[4], oc[2], ob[2];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { mc[k] = 0; mb[k] = 0; }
+        oc[0] = oc[1] = ob[0] = ob[1] = 0;
+    }
+    // one record per lane (the whole warp must call it)
+    __device__ __forceinline__ void add(bool valid, uint32_t cell, bool oow, uint32_t dir, uint64_t b) {
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            bool hit = valid && cell == k;
+            unsigned m = __ballot_sync(kFull, hit);
+            if (m) { mc[k] += (uint64_t)__popc(m); mb[k] += warp_sum_u64(hit ? b : 0ull); }
+        }
+#pragma unroll
+        for (uint32_t d = 0; d < 2; ++d) {
+            bool hit = oow && dir == d;
+            unsigned m = __ballot_sync(kFull, hit);
+            if (m) { oc[d] += (uint64_t)__popc(m); ob[d] += warp_sum_u64(hit ? b : 0ull); }
+        }
+    }
+};
+
+// Sum the per-warp totals of a block and add them to the global totals (one RED per counter).
+__device__ __forceinline__ void flush_totals(const WarpTotals& t, unsigned long long* g_totals,
+                                             unsigned long long* s_scratch /* [32][12] */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        unsigned long long* s = s_scratch + warp * 12;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { s[k] = t.mc[k]; s[4 + k] = t.mb[k]; }
+        s[8] = t.oc[0]; s[9] = t.oc[1]; s[10] = t.ob[0]; s[11] = t.ob[1];
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+        unsigned long long acc = 0;
+        for (int w = 0; w < nw; ++w) acc += s_scratch[w * 12 + threadIdx.x];
+        if (acc) atomicAdd(g_totals + threadIdx.x, acc);
+    }
+}
+
+// ---------------------------------------------------------------- a2: columnar record load
+struct Rec4 {
+    uint64_t ts[4];
+    uint32_t src[4], dst[4];
+    uint64_t by[4];
+};
+
+// Four consecutive records starting at `base` (base % 4 == 0): 6 x 128-bit
+// streaming loads when the group is complete, scalar loads for the tail.
+__device__ __forceinline__ void load4(const KernelParams& p, uint64_t base, Rec4& r) {
+    if (base + 4 <= p.n) {
+        ulonglong2 t0 = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + base));
+        ulonglong2 t1 = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + base + 2));
+        uint4 s = __ldcs(reinterpret_cast<const uint4*>(p.src + base));
+        uint4 d = __ldcs(reinterpret_cast<const uint4*>(p.dst + base));
+        ulonglong2 b0 = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + base));
+        ulonglong2 b1 = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + base + 2));
+        r.ts[0] = t0.x; r.ts[1] = t0.y; r.ts[2] = t1.x; r.ts[3] = t1.y;
+        r.src[0] = s.x; r.src[1] = s.y; r.src[2] = s.z; r.src[3] = s.w;
+        r.dst[0] = d.x; r.dst[1] = d.y; r.dst[2] = d.z; r.dst[3] = d.w;
+        r.by[0] = b0.x; r.by[1] = b0.y; r.by[2] = b1.x; r.by[3] = b1.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            bool ok = base + j < p.n;
+            r.ts[j] = ok ? p.ts[base + j] : 0ull;
+            r.src[j] = ok ? p.src[base + j] : 0u;
+            r.dst[j] = ok ? p.dst[base + j] : 0u;
+            r.by[j] = ok ? p.bytes[base + j] : 0ull;
+        }
+    }
+}
+
+__device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t base, uint32_t tag4) {
+    if (base + 4 <= p.n) {
+        *reinterpret_cast<uint32_t*>(p.tags + base) = tag4;
+    } else {
+        for (int j = 0; j < 4; ++j)
+            if (base + j < p.n) p.tags[base + j] = (uint8_t)(tag4 >> (8 * j));
+    }
+}
+
+// Stage the /16 class table (and small boundary arrays) into shared memory.
+__device__ __forceinline__ const uint32_t* stage_table(const KernelParams& p, uint32_t* s_cls2,
+                                                       uint32_t* s_bnd, bool bnd_in_smem) {
+    const uint4* g4 = reinterpret_cast<const uint4*>(p.cls2);
+    uint4* s4 = reinterpret_cast<uint4*>(s_cls2);
+    for (uint32_t i = threadIdx.x; i < kClsWords / 4; i += blockDim.x) s4[i] = __ldg(g4 + i);
+    if (bnd_in_smem) {
+        for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
+        return s_bnd;
+    }
+    return p.bnd;
+}
+
+}  // namespace sinet

@@ -1,0 +1,40 @@
+// Kernel parameter block and build constants shared by host launchers and device code.
+#pragma once
+#include <cstdint>
+
+namespace sinet {
+
+constexpr uint32_t kTileBins = 512;        // bins per claim tile (16 KB of u64[4] bins)
+constexpr uint32_t kClsWords = 4096;       // 65536 /16 blocks x 2 bits
+constexpr uint32_t kMaxSmemBnd = 4096;     // boundaries staged in shared memory up to this many
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// tile state word: epoch << 2 | state
+constexpr uint32_t kTileClaimed = 1u;
+constexpr uint32_t kTileInit = 2u;
+
+struct KernelParams {
+    const uint64_t* ts;
+    const uint32_t* src;
+    const uint32_t* dst;
+    const uint64_t* bytes;
+    uint64_t n;
+    uint8_t* tags;                 // nullable
+    unsigned long long* bins;      // u64 [B_pad][2 dir][2 metric]
+    unsigned long long* totals;    // 12 x u64
+    uint32_t* tile_flags;          // [n_tiles]
+    const uint32_t* cls2;          // [4096]
+    const uint32_t* entry;         // [65536]
+    const uint32_t* bnd;           // [nbnd]
+    uint32_t nbnd;
+    uint32_t lut;                  // 4 x 2 bits, index s_in*2+d_in
+    uint64_t start;                // window start (ms)
+    uint32_t window;               // W (ms) < 2^32
+    uint32_t width;                // w (ms)
+    uint32_t magic;                // floor(2^32 / w) for w >= 2
+    uint32_t nbins;                // B
+    uint32_t epoch;                // current epoch
+    uint32_t n_tiles;
+};
+
+}  // namespace sinet

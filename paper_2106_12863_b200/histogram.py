@@ -1,0 +1,228 @@
+"""User-facing Python API over libsinet (argument marshalling + torch-owned device memory).
+
+Every step of the hot path runs in the CUDA library; this module only
+allocates caller-owned buffers with torch, passes pointers and streams,
+and converts results.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import check, lib
+
+__all__ = ["SinetHistogram", "shard_range", "owned_bin_range", "padded_bins"]
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous record shard of rank `rank`: [rank*n//world, (rank+1)*n//world).
+
+    One file chunk per GPU thread in the paper becomes one
+    contiguous slice per rank."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def padded_bins(nbins: int, world: int, tile_bins: int | None = None) -> int:
+    t = int(lib.sinet_tile_bins()) if tile_bins is None else tile_bins
+    unit = world * t
+    return (nbins + unit - 1) // unit * unit
+
+
+def owned_bin_range(nbins: int, rank: int, world: int, tile_bins: int | None = None):
+    """Bins rank `rank` holds after the reduce-scatter: [lo, hi) clipped to [0, nbins)."""
+    per = padded_bins(nbins, world, tile_bins) // world
+    lo, hi = min(per * rank, nbins), min(per * (rank + 1), nbins)
+    return lo, hi
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+class SinetHistogram:
+    """One per (process, GPU): the compiled CIDR list, the bins and the totals.
+
+    nets/lens: the CIDR list (Y.Y.Y.Y as u32, Z), Alg. 1 l.1,4.
+    Bins: u64 [B_pad][2 dir][2 metric], one 32-byte sector per ms bin.
+    """
+
+    def __init__(self, nets, lens, window_start_ms: int, window_ms: int, bin_width_ms: int = 1,
+                 lut=N.LUT_SRC_PRIORITY, device=None, rank: int = 0, world: int = 1,
+                 stream: torch.cuda.Stream | None = None, order: int = N.ORDER_AUTO):
+        if not torch.cuda.is_available():
+            raise RuntimeError("SinetHistogram needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        cfg = N.Config()
+        cfg.window_start_ms = int(window_start_ms)
+        cfg.window_ms = int(window_ms)
+        cfg.bin_width_ms = int(bin_width_ms)
+        for k in range(4):
+            cfg.dir_lut[k] = int(lut[k])
+        cfg.device = self.device.index
+        cfg.rank, cfg.world = int(rank), int(world)
+        cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        cfg.order_hint = int(order)
+        self.cfg = cfg
+        self.nbins = int(window_ms) // int(bin_width_ms)
+        self.rank, self.world = int(rank), int(world)
+        nets = np.ascontiguousarray(np.asarray(nets, dtype=np.uint32))
+        lens = np.ascontiguousarray(np.asarray(lens, dtype=np.uint8))
+        bb = lib.sinet_bins_bytes(ctypes.byref(cfg))
+        wb = lib.sinet_workspace_bytes(ctypes.byref(cfg), len(nets))
+        if bb == 0 or wb == 0:
+            raise N.SinetError(N.E_INVAL, "invalid configuration or prefix count")
+        self.B_pad = bb // 32
+        with torch.cuda.device(self.device):
+            self.bins = torch.empty(bb // 8, dtype=torch.int64, device=self.device)
+            self.ws = torch.empty(wb, dtype=torch.uint8, device=self.device)
+        ctx = ctypes.c_void_p()
+        rc = lib.sinet_open(ctypes.byref(ctx), ctypes.byref(cfg), nets.ctypes.data_as(ctypes.c_void_p),
+                            lens.ctypes.data_as(ctypes.c_void_p), len(nets), _ptr(self.bins), bb,
+                            _ptr(self.ws), wb)
+        check(rc, None, "sinet_open")
+        self.ctx = ctx
+        self._staging = None
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.sinet_close(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def reset(self):
+        check(lib.sinet_reset(self.ctx), self.ctx, "reset")
+
+    # ------------------------------------------------------------------ hot path
+    @staticmethod
+    def _records(ts, src, dst, nbytes):
+        n = ts.numel()
+        assert src.numel() == n and dst.numel() == n and nbytes.numel() == n
+        assert ts.element_size() == 8 and nbytes.element_size() == 8
+        assert src.element_size() == 4 and dst.element_size() == 4
+        for t in (ts, src, dst, nbytes):
+            assert t.is_contiguous()
+        return N.Records(ts.data_ptr(), src.data_ptr(), dst.data_ptr(), nbytes.data_ptr(), n)
+
+    def classify(self, ts, src, dst, nbytes, tags: torch.Tensor | None = None):
+        """Accumulate one batch of device-resident records (int64/int32 bit patterns)."""
+        for t in (ts, src, dst, nbytes):
+            assert t.device == self.device, "records must live on the ctx device"
+        recs = self._records(ts, src, dst, nbytes)
+        if tags is not None:
+            assert tags.dtype == torch.uint8 and tags.numel() >= ts.numel() and tags.device == self.device
+        check(lib.sinet_classify_histogram(self.ctx, ctypes.byref(recs), _ptr(tags)), self.ctx, "classify")
+
+    def classify_host(self, ts, src, dst, nbytes, chunk_records: int = 1 << 24):
+        """Accumulate host (ideally pinned) records, streamed through a device staging buffer."""
+        for t in (ts, src, dst, nbytes):
+            assert t.device.type == "cpu"
+        need = lib.sinet_staging_bytes(chunk_records)
+        if self._staging is None or self._staging.numel() < need:
+            self._staging = torch.empty(need, dtype=torch.uint8, device=self.device)
+        recs = self._records(ts, src, dst, nbytes)
+        check(lib.sinet_classify_histogram_host(self.ctx, ctypes.byref(recs), _ptr(self._staging), need,
+                                                chunk_records), self.ctx, "classify_host")
+
+    def finalize(self):
+        check(lib.sinet_finalize(self.ctx), self.ctx, "finalize")
+
+    # ------------------------------------------------------------------ multi-GPU
+    @staticmethod
+    def new_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib.sinet_nccl_unique_id(buf), None, "nccl unique id")
+        return buf.raw
+
+    def comm_init(self, unique_id: bytes):
+        assert len(unique_id) == 128
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        check(lib.sinet_comm_init(self.ctx, buf), self.ctx, "comm_init")
+
+    def comm_init_from_group(self, group=None):
+        """Rank 0 creates the NCCL id; torch.distributed broadcasts it (plumbing only)."""
+        import torch.distributed as dist
+        obj = [self.new_unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.comm_init(obj[0])
+
+    def reduce(self):
+        check(lib.sinet_reduce(self.ctx), self.ctx, "reduce")
+
+    def owned_range(self):
+        lo, n = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.sinet_owned_range(self.ctx, ctypes.byref(lo), ctypes.byref(n)), self.ctx, "owned_range")
+        return lo.value, lo.value + n.value
+
+    # ------------------------------------------------------------------ read-out
+    def read_bins(self, direction: int, metric: int, first: int = 0, n: int | None = None,
+                  device: bool = False):
+        """u64 plane slice as numpy uint64 (host) or a torch int64 tensor (device)."""
+        lo, hi = self.owned_range()
+        if n is None:
+            n = hi - first
+        if device:
+            out = torch.empty(n, dtype=torch.int64, device=self.device)
+            ptr = _ptr(out)
+        else:
+            out = np.empty(n, dtype=np.uint64)
+            ptr = out.ctypes.data_as(ctypes.c_void_p)
+        check(lib.sinet_read_bins(self.ctx, direction, metric, first, n, ptr, 1 if device else 0),
+              self.ctx, "read_bins")
+        return out
+
+    def read_totals(self) -> np.ndarray:
+        """12 x u64: m_count[4], m_bytes[4], oow_count[2], oow_bytes[2] (oracle layout)."""
+        t = N.Totals()
+        check(lib.sinet_read_totals(self.ctx, ctypes.byref(t)), self.ctx, "read_totals")
+        return np.array(list(t.m_count) + list(t.m_bytes) + list(t.oow_count) + list(t.oow_bytes),
+                        dtype=np.uint64)
+
+    def bins_view(self) -> torch.Tensor:
+        """Device view int64[B_pad, 2, 2] of the bins buffer (after finalize/reduce)."""
+        return self.bins.view(self.B_pad, 2, 2)
+
+    # ------------------------------------------------------------------ introspection
+    @property
+    def launches(self) -> int:
+        return int(lib.sinet_launch_count(self.ctx))
+
+    @property
+    def last_strategy(self) -> int:
+        return int(lib.sinet_last_strategy(self.ctx))
+
+    def set_kernel_timing(self, on: bool):
+        check(lib.sinet_set_kernel_timing(self.ctx, 1 if on else 0), self.ctx, "timing")
+
+    def kernel_time(self):
+        ms, k = ctypes.c_double(), ctypes.c_uint64()
+        check(lib.sinet_kernel_time(self.ctx, ctypes.byref(ms), ctypes.byref(k)), self.ctx, "kernel_time")
+        return ms.value, k.value
+
+
+def table_member_host(nets, lens, ips) -> np.ndarray:
+    """Host evaluation of the compiled lookup table (prefix compiler check, no GPU)."""
+    nets = np.ascontiguousarray(np.asarray(nets, dtype=np.uint32))
+    lens = np.ascontiguousarray(np.asarray(lens, dtype=np.uint8))
+    ips = np.ascontiguousarray(np.asarray(ips, dtype=np.uint32))
+    out = np.empty(len(ips), dtype=np.uint8)
+    rc = lib.sinet_table_member_host(nets.ctypes.data_as(ctypes.c_void_p), lens.ctypes.data_as(ctypes.c_void_p),
+                                     len(nets), ips.ctypes.data_as(ctypes.c_void_p), len(ips),
+                                     out.ctypes.data_as(ctypes.c_void_p))
+    check(rc, None, "table_member_host")
+    return out

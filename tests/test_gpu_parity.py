@@ -1,0 +1,213 @@
+"""GPU parity: libsinet (through its C ABI) vs the CPU oracle, bit-exact.
+
+All arithmetic on the path is integer, so the bar is exact equality of every
+bin, every total and every tag.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.core import LUT_ALG1, LUT_SRC_PRIORITY, LUT_STRICT
+from synth import WORKLOADS, prefix_table, records
+from synth.sinet_synth import to_numpy
+from tests.helpers import edge_addresses, load_f0
+
+pytestmark = pytest.mark.gpu
+
+ORDERS = None
+
+
+@pytest.fixture(scope="module")
+def S():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2106_12863_b200 as S
+    return S
+
+
+def dev_cols(cols, device="cuda"):
+    ts, src, dst, nb = cols
+    return (torch.from_numpy(np.ascontiguousarray(ts).view(np.int64)).to(device),
+            torch.from_numpy(np.ascontiguousarray(src).view(np.int32)).to(device),
+            torch.from_numpy(np.ascontiguousarray(dst).view(np.int32)).to(device),
+            torch.from_numpy(np.ascontiguousarray(nb).view(np.int64)).to(device))
+
+
+def gpu_run(S, nets, lens, cols, start, window, width=1, lut=LUT_SRC_PRIORITY, order=0, chunks=None,
+            tags=False):
+    h = S.SinetHistogram(nets, lens, start, window, width, lut=lut, order=order)
+    d = dev_cols(cols)
+    n = d[0].numel()
+    tg = torch.full((max(n, 4),), 0xEE, dtype=torch.uint8, device="cuda") if tags else None
+    if chunks is None:
+        h.classify(*d, tags=tg)
+    else:
+        for lo, hi in chunks:
+            h.classify(*(c[lo:hi] for c in d), tags=None if tg is None else tg[lo:hi])
+    out = {"count": np.stack([h.read_bins(k, S.METRIC_COUNT) for k in (0, 1)]),
+           "bytes": np.stack([h.read_bins(k, S.METRIC_BYTES) for k in (0, 1)]),
+           "totals": h.read_totals(), "h": h}
+    if tags:
+        out["tags"] = tg[:n].cpu().numpy()
+    return out
+
+
+def assert_parity(g, o):
+    np.testing.assert_array_equal(g["count"], o.count)
+    np.testing.assert_array_equal(g["bytes"], o.bytes)
+    np.testing.assert_array_equal(g["totals"], o.totals)
+
+
+@pytest.mark.parametrize("case", ["src_priority_w1", "alg1_w1", "strict_w1", "src_priority_w5"])
+def test_f0_golden_on_gpu(S, oracle_lib, case):
+    g, nets, lens, ts, src, dst, nb = load_f0()
+    e = g["expected"][case]
+    cols = (ts, src, dst, nb)
+    res = gpu_run(S, nets, lens, cols, g["window_start_ms"], g["window_ms"], e["width"], tuple(e["lut"]),
+                  tags=True)
+    o = oracle_lib.classify_histogram(*cols, nets, lens, g["window_start_ms"], g["window_ms"], e["width"],
+                                      lut=tuple(e["lut"]))
+    assert_parity(res, o)
+    np.testing.assert_array_equal(res["tags"], oracle_lib.tags(ts, src, dst, nets, lens, g["window_start_ms"],
+                                                               g["window_ms"]))
+
+
+def _adversarial(n, nets, lens, start, window, seed):
+    rng = np.random.default_rng(seed)
+    edges = edge_addresses(nets, lens)
+    pick = lambda: np.where(rng.random(n) < 0.4, rng.choice(edges, n),
+                            rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)).astype(np.uint32)
+    ts = (start + rng.integers(-300, window + 300, n)).astype(np.uint64)
+    nb = rng.integers(0, 1 << 40, n, dtype=np.uint64)
+    big = rng.random(n) < 0.02
+    nb[big] = rng.integers(1 << 62, 1 << 63, int(big.sum()), dtype=np.uint64) * np.uint64(2)
+    return ts, pick(), pick(), nb
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("lut", [LUT_SRC_PRIORITY, LUT_ALG1, LUT_STRICT])
+@pytest.mark.parametrize("width", [1, 3, 1000])
+def test_adversarial_parity(S, oracle_lib, lut, width, order):
+    nets, lens = prefix_table(WORKLOADS["c1"])
+    start, window = 1_613_660_400_000, 3_000_000
+    for n in (1, 5, 127, 129, 40_001):   # ragged tails around the 4-record / 128-record groups
+        cols = _adversarial(n, nets, lens, start, window, seed=n + width)
+        g = gpu_run(S, nets, lens, cols, start, window, width, lut, order=order, tags=True)
+        o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, width, lut=lut)
+        assert_parity(g, o)
+        np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
+                                                                 start, window))
+
+
+@pytest.mark.parametrize("wl_name,order", [("c1", "stream"), ("c1", "shuffled")])
+def test_c1_full_parity(S, oracle_lib, wl_name, order):
+    """BASELINE configs[0] at full size: 1M sessions, 1 h of 1 ms bins, 16 prefixes."""
+    wl = WORKLOADS[wl_name].with_(order=order)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    for strategy in (0, 1, 2):
+        g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy)
+        o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+        assert_parity(g, o)
+
+
+def test_chunked_accumulation_and_reset(S, oracle_lib):
+    wl = WORKLOADS["c1"].with_(n=300_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms,
+                chunks=[(0, 4), (4, 1001), (1001, 1001), (1001, 250_000), (250_000, 300_000)])
+    assert_parity(g, o)
+    h = g["h"]
+    # reset: a new epoch starts empty; re-running gives the same result (bins not re-zeroed by memset)
+    h.reset()
+    z = h.read_totals()
+    assert not z.any()
+    assert not h.read_bins(0, 0).any() and not h.read_bins(1, 1).any()
+    d = dev_cols(cols)
+    for _ in range(2):
+        h.reset()
+        h.classify(*d)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count)
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
+
+
+def test_empty_input_and_errors(S):
+    nets, lens = prefix_table(WORKLOADS["c1"])
+    h = S.SinetHistogram(nets, lens, 1000, 100, 1)
+    e64 = torch.empty(0, dtype=torch.int64, device="cuda")
+    e32 = torch.empty(0, dtype=torch.int32, device="cuda")
+    h.classify(e64, e32, e32, e64)
+    assert not h.read_totals().any() and not h.read_bins(0, 0).any()
+    x64 = torch.zeros(9, dtype=torch.int64, device="cuda")
+    x32 = torch.zeros(9, dtype=torch.int32, device="cuda")
+    with pytest.raises(S.SinetError) as ei:
+        h.classify(x64[1:], x32[1:], x32[1:], x64[1:])   # misaligned columns
+    assert ei.value.code == -2
+    with pytest.raises(S.SinetError) as ei:
+        h.read_bins(0, 0, first=50, n=51)
+    assert ei.value.code == -3
+    h.reduce()
+    with pytest.raises(S.SinetError) as ei:
+        h.classify(x64[:8], x32[:8], x32[:8], x64[:8])
+    assert ei.value.code == -6
+    h.reset()
+    h.classify(x64[:8], x32[:8], x32[:8], x64[:8])
+
+
+def test_host_streaming_path(S, oracle_lib):
+    wl = WORKLOADS["c1"].with_(n=500_000)
+    nets, lens = prefix_table(wl)
+    rec = records(wl)
+    cols = to_numpy(rec)
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms)
+    pin = [rec[k].pin_memory() for k in ("ts", "src", "dst", "bytes")]
+    h.classify_host(*pin, chunk_records=65_536 + 4)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
+
+
+def test_reduce_single_rank_is_identity(S, oracle_lib):
+    wl = WORKLOADS["c1"].with_(n=100_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms)
+    h.classify(*dev_cols(cols))
+    h.reduce()
+    assert h.owned_range() == (0, wl.nbins)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count)
+
+
+def test_generator_cpu_gpu_identical(S):
+    for name in ("c1", "c4"):
+        wl = WORKLOADS[name].with_(n=200_000)
+        a = records(wl, 1000, 150_000, device="cpu")
+        b = records(wl, 1000, 150_000, device="cuda")
+        for k in a:
+            assert torch.equal(a[k], b[k].cpu()), (name, k)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("strategy", [0, 2])
+def test_c2_full_size_parity(S, oracle_lib, strategy):
+    """BASELINE configs[1] at full size (100M sessions, one day of 1 ms bins, 64
+    prefixes), in the bench's launch configuration, every bin vs the oracle."""
+    wl = WORKLOADS["c2"]
+    nets, lens = prefix_table(wl)
+    rec = records(wl, device="cuda")
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, order=strategy)
+    h.classify(rec["ts"], rec["src"], rec["dst"], rec["bytes"])
+    h.finalize()
+    cols = tuple(c for c in to_numpy({k: rec[k].cpu() for k in rec}))
+    del rec
+    torch.cuda.empty_cache()
+    import os
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1,
+                                      threads=max(1, len(os.sched_getaffinity(0))))
+    for d in (0, 1):
+        np.testing.assert_array_equal(h.read_bins(d, 0), o.count[d])
+        np.testing.assert_array_equal(h.read_bins(d, 1), o.bytes[d])
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
