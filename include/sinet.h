@@ -45,7 +45,7 @@ extern "C" {
 /* error codes */
 #define SINET_OK        0
 #define SINET_E_INVAL  -1   /* invalid argument (see each call) */
-#define SINET_E_ALIGN  -2   /* a device column base is not 16-byte aligned */
+#define SINET_E_ALIGN  -2   /* device columns misaligned (see sinet_records) */
 #define SINET_E_RANGE  -3   /* bin range outside [0,B) or outside this rank's owned range after reduce */
 #define SINET_E_CUDA   -4   /* CUDA runtime error (asynchronous errors surface at the next synchronising call) */
 #define SINET_E_NCCL   -5   /* NCCL unavailable or failed */
@@ -68,8 +68,10 @@ extern "C" {
 typedef struct sinet_ctx sinet_ctx;
 
 /* One batch ("chunk") of session records, columnar.
- * Device pointers for sinet_classify_histogram (each base 16-byte aligned),
- * host pointers for sinet_classify_histogram_host.  n may be 0.           */
+ * Device pointers for sinet_classify_histogram: naturally aligned, and all four
+ * columns starting at the same record offset within a 16-byte group (true for
+ * any slice [i, j) of 16-byte aligned columns); host pointers for
+ * sinet_classify_histogram_host.  n may be 0.                              */
 typedef struct {
     const uint64_t* ts_ms;   /* capture_time, epoch milliseconds (Table 1 no. 1) */
     const uint32_t* src;     /* source_ip (no. 5) */
@@ -146,7 +148,7 @@ int sinet_reset(sinet_ctx* ctx);
  * count and bytes into its (bin, dir).  Calling it on k batches
  * equals calling it once on their concatenation (work queue chunks).
  * d_tags (nullable, device, n bytes): per-record tag s_in | d_in<<1 | oow<<2.
- * Errors: E_INVAL (NULL column with n > 0), E_ALIGN, E_STATE (after reduce
+ * Errors: E_INVAL (NULL column with n > 0), E_ALIGN (see sinet_records), E_STATE (after reduce
  * without reset), E_CUDA (launch failure). */
 int sinet_classify_histogram(sinet_ctx* ctx, const sinet_records* recs, uint8_t* d_tags);
 

@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -123,6 +125,8 @@ struct sinet_ctx {
     bool reduced = false;
     bool materialized = false;
     int last_strategy = 0;
+    int auto_choice = 0;          // strategy AUTO resolved by the first probe
+    bool agg = true;              // warp aggregation of equal keys in the stream kernel
     uint64_t launches = 0;
     ncclComm_t comm = nullptr;
     // host-streaming pipeline
@@ -199,37 +203,83 @@ int do_materialize(sinet_ctx* c) {
     return SINET_OK;
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// Strategy AUTO: look at 64 evenly spaced runs of 32 consecutive capture times.
+// Time-ordered logs (day files processed chunk by chunk) have runs that
+// span about the capture disorder; shuffled input spans the whole window.
+int probe_order(sinet_ctx* c, const sinet_records* r, int* out) {
+    constexpr int kRuns = 64, kRun = 32;
+    if (r->n < (uint64_t)kRuns * kRun) { *out = SINET_ORDER_STREAM; return SINET_OK; }
+    std::vector<uint64_t> h((size_t)kRuns * kRun);
+    for (int k = 0; k < kRuns; ++k) {
+        const uint64_t at = (r->n - kRun) * (uint64_t)k / (kRuns - 1);
+        SINET_CUDA(c, cudaMemcpyAsync(h.data() + (size_t)k * kRun, r->ts_ms + at, kRun * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    std::vector<uint64_t> span(kRuns);
+    for (int k = 0; k < kRuns; ++k) {
+        uint64_t lo = ~0ull, hi = 0;
+        for (int i = 0; i < kRun; ++i) { uint64_t v = h[(size_t)k * kRun + i]; lo = v < lo ? v : lo; hi = v > hi ? v : hi; }
+        span[k] = hi - lo;
+    }
+    std::nth_element(span.begin(), span.begin() + kRuns / 2, span.end());
+    const uint64_t limit = (uint64_t)kStreamWindowBins / 2 * c->cfg.bin_width_ms;
+    *out = (span[kRuns / 2] <= limit) ? SINET_ORDER_STREAM : SINET_ORDER_SHUFFLED;
+    return SINET_OK;
+}
 
 int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
     if (c->reduced) return fail(c, SINET_E_STATE, "classify after reduce: call sinet_reset first");
     if (!r) return fail(c, SINET_E_INVAL, "NULL records");
     if (r->n == 0) return SINET_OK;
+    if (r->n > (1ull << 38)) return fail(c, SINET_E_INVAL, "batch larger than 2^38 records: split it");
     if (!r->ts_ms || !r->src || !r->dst || !r->bytes) return fail(c, SINET_E_INVAL, "NULL record column");
-    if (!aligned16(r->ts_ms) || !aligned16(r->src) || !aligned16(r->dst) || !aligned16(r->bytes))
-        return fail(c, SINET_E_ALIGN, "record columns must be 16-byte aligned");
-    if (d_tags && (reinterpret_cast<uintptr_t>(d_tags) & 3u))
-        return fail(c, SINET_E_ALIGN, "tags buffer must be 4-byte aligned");
+    // Columns may start mid-way into a 16-byte group (e.g. a batch sliced at any
+    // record index) as long as all four are offset by the same number of records.
+    const uintptr_t a_ts = reinterpret_cast<uintptr_t>(r->ts_ms), a_src = reinterpret_cast<uintptr_t>(r->src),
+                    a_dst = reinterpret_cast<uintptr_t>(r->dst), a_by = reinterpret_cast<uintptr_t>(r->bytes);
+    const uint32_t head = (uint32_t)((a_src & 15u) >> 2);
+    if ((a_ts & 7u) || (a_by & 7u) || (a_src & 3u) || (a_dst & 3u) || ((a_dst & 15u) >> 2) != head ||
+        ((a_ts - 8u * head) & 15u) || ((a_by - 8u * head) & 15u))
+        return fail(c, SINET_E_ALIGN, "record columns must be naturally aligned and start at the same "
+                                      "record offset within a 16-byte group (16-byte aligned bases)");
     KernelParams p = base_params(c);
     p.ts = r->ts_ms; p.src = r->src; p.dst = r->dst; p.bytes = r->bytes; p.n = r->n; p.tags = d_tags;
+    p.head = head;
+    p.nv = r->n + head;
+    p.tags_vec = d_tags && (((reinterpret_cast<uintptr_t>(d_tags) - head) & 3u) == 0) ? 1u : 0u;
 
-    // strategy SHUFFLED (v0): materialise every tile, then L2 atomics
-    int rc = do_materialize(c);
-    if (rc) return rc;
+    int strategy = (int)c->cfg.order_hint;
+    if (strategy == SINET_ORDER_AUTO) {
+        if (!c->auto_choice) {
+            int rc = probe_order(c, r, &c->auto_choice);
+            if (rc) return rc;
+        }
+        strategy = c->auto_choice;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (strategy == SINET_ORDER_SHUFFLED) {
+        // materialise every tile, then L2 atomics (any order)
+        int rc = do_materialize(c);
+        if (rc) return rc;
+    }
     if (c->timing) {
         SINET_CUDA(c, cudaEventCreate(&e0));
         SINET_CUDA(c, cudaEventCreate(&e1));
         SINET_CUDA(c, cudaEventRecord(e0, c->stream));
     }
-    SINET_CUDA(c, launch_hist_atomic(p, c->atomic_grid, c->stream));
+    if (strategy == SINET_ORDER_SHUFFLED) {
+        SINET_CUDA(c, launch_hist_atomic(p, c->atomic_grid, c->stream));
+    } else {
+        // time-window privatisation, write-once bins; untouched tiles stay virtual
+        SINET_CUDA(c, launch_hist_stream(p, c->sm_count, c->agg, c->stream));
+        c->materialized = false;
+    }
     c->launches++;
-    c->last_strategy = SINET_ORDER_SHUFFLED;
+    c->last_strategy = strategy;
     if (c->timing) {
         SINET_CUDA(c, cudaEventRecord(e1, c->stream));
         c->tev.emplace_back(e0, e1);
     }
-    // bins stay materialised: atomics only add to initialised tiles
     return SINET_OK;
 }
 
@@ -297,6 +347,8 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     if ((e = (expr)) != cudaSuccess) { std::fprintf(stderr, "sinet_open: %s: %s\n", #expr, cudaGetErrorString(e)); return bail(SINET_E_CUDA); }
     OPEN_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
     OPEN_CUDA(setup_hist_atomic());
+    OPEN_CUDA(setup_hist_stream());
+    if (const char* a = std::getenv("SINET_AGG")) c->agg = std::atoi(a) != 0;
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(c->nbnd);
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states

@@ -101,16 +101,23 @@ struct Rec4 {
     uint64_t by[4];
 };
 
-// Four consecutive records starting at `base` (base % 4 == 0): 6 x 128-bit
-// streaming loads when the group is complete, scalar loads for the tail.
-__device__ __forceinline__ void load4(const KernelParams& p, uint64_t base, Rec4& r) {
-    if (base + 4 <= p.n) {
-        ulonglong2 t0 = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + base));
-        ulonglong2 t1 = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + base + 2));
-        uint4 s = __ldcs(reinterpret_cast<const uint4*>(p.src + base));
-        uint4 d = __ldcs(reinterpret_cast<const uint4*>(p.dst + base));
-        ulonglong2 b0 = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + base));
-        ulonglong2 b1 = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + base + 2));
+// Four consecutive records of the virtual (16-byte aligned) index space,
+// starting at virtual index vbase (vbase % 4 == 0): record vbase + j is column
+// element vbase + j - head.  Complete groups use 6 x 128-bit streaming loads;
+// the ragged first and last groups use scalar loads.
+__device__ __forceinline__ bool vvalid(const KernelParams& p, uint64_t v) {
+    return v >= p.head && v < p.nv;
+}
+
+__device__ __forceinline__ void load4(const KernelParams& p, uint64_t vbase, Rec4& r) {
+    if (vbase >= p.head && vbase + 4 <= p.nv) {
+        const uint64_t a = vbase - p.head;
+        ulonglong2 t0 = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + a));
+        ulonglong2 t1 = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + a + 2));
+        uint4 s = __ldcs(reinterpret_cast<const uint4*>(p.src + a));
+        uint4 d = __ldcs(reinterpret_cast<const uint4*>(p.dst + a));
+        ulonglong2 b0 = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + a));
+        ulonglong2 b1 = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + a + 2));
         r.ts[0] = t0.x; r.ts[1] = t0.y; r.ts[2] = t1.x; r.ts[3] = t1.y;
         r.src[0] = s.x; r.src[1] = s.y; r.src[2] = s.z; r.src[3] = s.w;
         r.dst[0] = d.x; r.dst[1] = d.y; r.dst[2] = d.z; r.dst[3] = d.w;
@@ -118,21 +125,22 @@ __device__ __forceinline__ void load4(const KernelParams& p, uint64_t base, Rec4
     } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            bool ok = base + j < p.n;
-            r.ts[j] = ok ? p.ts[base + j] : 0ull;
-            r.src[j] = ok ? p.src[base + j] : 0u;
-            r.dst[j] = ok ? p.dst[base + j] : 0u;
-            r.by[j] = ok ? p.bytes[base + j] : 0ull;
+            const bool ok = vvalid(p, vbase + j);
+            const uint64_t a = vbase + j - p.head;
+            r.ts[j] = ok ? p.ts[a] : 0ull;
+            r.src[j] = ok ? p.src[a] : 0u;
+            r.dst[j] = ok ? p.dst[a] : 0u;
+            r.by[j] = ok ? p.bytes[a] : 0ull;
         }
     }
 }
 
-__device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t base, uint32_t tag4) {
-    if (base + 4 <= p.n) {
-        *reinterpret_cast<uint32_t*>(p.tags + base) = tag4;
+__device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t vbase, uint32_t tag4) {
+    if (p.tags_vec && vbase >= p.head && vbase + 4 <= p.nv) {
+        *reinterpret_cast<uint32_t*>(p.tags + (vbase - p.head)) = tag4;
     } else {
         for (int j = 0; j < 4; ++j)
-            if (base + j < p.n) p.tags[base + j] = (uint8_t)(tag4 >> (8 * j));
+            if (vvalid(p, vbase + j)) p.tags[vbase + j - p.head] = (uint8_t)(tag4 >> (8 * j));
     }
 }
 

@@ -54,14 +54,14 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
     WarpTotals tot;
     tot.zero();
 
-    for (uint64_t wbase = gw * 128ull; wbase < p.n; wbase += stride) {
+    for (uint64_t wbase = gw * 128ull; wbase < p.nv; wbase += stride) {
         const uint64_t base = wbase + lane * 4ull;
         Rec4 r;
         load4(p, base, r);
         uint32_t tag4 = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const bool valid = base + j < p.n;
+            const bool valid = vvalid(p, base + j);
             const uint32_t s_in = member(r.src[j], s_cls2, p.entry, bnd);
             const uint32_t d_in = member(r.dst[j], s_cls2, p.entry, bnd);
             const uint32_t cell = s_in * 2u + d_in;

@@ -16,4 +16,8 @@ cudaError_t setup_hist_atomic();
 int hist_atomic_blocks_per_sm(uint32_t nbnd);
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st);
 
+cudaError_t setup_hist_stream();
+cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st);
+constexpr uint32_t kStreamWindowBins = 8192;
+
 }  // namespace sinet

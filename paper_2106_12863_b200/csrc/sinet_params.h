@@ -18,7 +18,10 @@ struct KernelParams {
     const uint32_t* src;
     const uint32_t* dst;
     const uint64_t* bytes;
-    uint64_t n;
+    uint64_t n;                    // records in this batch
+    uint64_t nv;                   // n + head: records in "virtual" 16-byte-aligned index space
+    uint32_t head;                 // columns start `head` records past a 16-byte boundary (0..3)
+    uint32_t tags_vec;             // 1 if tags - head is 4-byte aligned (u32 tag stores)
     uint8_t* tags;                 // nullable
     unsigned long long* bins;      // u64 [B_pad][2 dir][2 metric]
     unsigned long long* totals;    // 12 x u64

@@ -111,6 +111,42 @@ def test_c1_full_parity(S, oracle_lib, wl_name, order):
         assert_parity(g, o)
 
 
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_bursty_hot_bins(S, oracle_lib, strategy):
+    """C4-shaped (diurnal + Zipf bursts + 1 % in one ms) and a degenerate all-in-one-ms batch."""
+    wl = WORKLOADS["c4"].with_(n=2_000_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy)
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    assert_parity(g, o)
+    ts, src, dst, nb = cols
+    one = (np.full_like(ts, wl.window_start_ms + 43_200_000), src, dst, nb)
+    g = gpu_run(S, nets, lens, one, wl.window_start_ms, wl.window_ms, order=strategy)
+    o = oracle_lib.classify_histogram(*one, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_gaps_and_window_jumps(S, oracle_lib, strategy):
+    """Sparse records hours apart (window jumps), then a dense stretch, in one batch."""
+    rng = np.random.default_rng(77)
+    nets, lens = prefix_table(WORKLOADS["c2"])
+    start, window = 1_613_660_400_000, 86_400_000
+    sparse = np.sort(rng.integers(0, window, 3000))
+    dense = 40_000_000 + np.sort(rng.integers(0, 60_000, 200_000))
+    off = np.concatenate([sparse[:1500], dense, sparse[1500:]])
+    n = len(off)
+    ts = (start + off).astype(np.uint64)
+    src = rng.choice(np.concatenate([nets, rng.integers(0, 1 << 32, 64).astype(np.uint32)]), n).astype(np.uint32)
+    dst = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    nb = rng.integers(0, 1 << 34, n, dtype=np.uint64)
+    cols = (ts, src, dst, nb)
+    g = gpu_run(S, nets, lens, cols, start, window, order=strategy)
+    o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, 1)
+    assert_parity(g, o)
+
+
 def test_chunked_accumulation_and_reset(S, oracle_lib):
     wl = WORKLOADS["c1"].with_(n=300_000)
     nets, lens = prefix_table(wl)
@@ -143,8 +179,9 @@ def test_empty_input_and_errors(S):
     x64 = torch.zeros(9, dtype=torch.int64, device="cuda")
     x32 = torch.zeros(9, dtype=torch.int32, device="cuda")
     with pytest.raises(S.SinetError) as ei:
-        h.classify(x64[1:], x32[1:], x32[1:], x64[1:])   # misaligned columns
+        h.classify(x64[1:], x32[:8], x32[:8], x64[1:])   # columns at different record offsets
     assert ei.value.code == -2
+    h.classify(x64[1:], x32[1:], x32[1:], x64[1:])       # same offset (a slice): accepted
     with pytest.raises(S.SinetError) as ei:
         h.read_bins(0, 0, first=50, n=51)
     assert ei.value.code == -3
