@@ -1,0 +1,12 @@
+set -x
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q --durations=8 > gpurun_out/pytest_gpu.txt 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_stream.txt 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --strategy shuffled > gpurun_out/bench_shufstrat.txt 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --order shuffled > gpurun_out/bench_shuforder.txt 2>&1
+SINET_AGG=0 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_noagg.txt 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --config c4 --records-per-gpu 400000000 > gpurun_out/bench_c4_400m.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --profile > gpurun_out/ncu_launch_run.txt 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o gpurun_out/prof_stream python bench.py --steps 2 --warmup 1 --profile > gpurun_out/ncu_full_run.txt 2>&1
+tail -n 3 gpurun_out/*.txt
