@@ -193,6 +193,23 @@ int sinet_owned_range(sinet_ctx* ctx, uint64_t* first_bin, uint64_t* n_bins);
 int sinet_read_bins(sinet_ctx* ctx, int dir, int metric, uint64_t first_bin, uint64_t n_bins,
                     uint64_t* dst, int dst_is_device);
 
+/* NEXT-1, coarser frames: "Session data is grouped into one-hour frame bins"
+ * (P:L323); "about 40,000 in 10 minutes".  Sums every `factor`
+ * consecutive bins of the owned range [lo, lo+n) into
+ * d_out u64[n_out][2 dir][2 metric] (device, 8-byte aligned), coarse bin k =
+ * bins [lo + k*factor, min(lo + (k+1)*factor, lo+n)); n_out must equal
+ * ceil(n / factor).  u64 sums wrap mod 2^64.  Errors: E_INVAL, E_CUDA. */
+int sinet_rebin(sinet_ctx* ctx, uint64_t factor, uint64_t* d_out, uint64_t n_out);
+
+/* NEXT-1, sparse series: the key/value namespaces X1<timestamp>, X1<count>,
+ * X2<timestamp>, X2<bytes>.  Writes, in ascending bin order,
+ * (bin start in epoch ms, count, bytes) of every bin of direction `dir` in the
+ * owned range whose count is nonzero, at most `capacity` entries, into device
+ * arrays u64[capacity]; *n_nonzero (host) receives the total number of such
+ * bins (may exceed capacity).  Synchronises the stream.  Errors: E_INVAL, E_CUDA. */
+int sinet_export_sparse(sinet_ctx* ctx, int dir, uint64_t* d_ts_ms, uint64_t* d_count, uint64_t* d_bytes,
+                        uint64_t capacity, uint64_t* n_nonzero);
+
 /* Copy the totals to host (synchronises the stream). */
 int sinet_read_totals(sinet_ctx* ctx, sinet_totals* out);
 

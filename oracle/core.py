@@ -58,6 +58,11 @@ def _load():
         lib.oracle_tags.argtypes = [u64p, u32p, u32p, ctypes.c_uint64, u32p, u8p, ctypes.c_uint32,
                                     ctypes.c_uint64, ctypes.c_uint64, u8p]
         lib.oracle_tags.restype = None
+        lib.oracle_rebin.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, u64p]
+        lib.oracle_rebin.restype = None
+        lib.oracle_sparse.argtypes = [u64p, u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                                      u64p, u64p, u64p, ctypes.c_uint64]
+        lib.oracle_sparse.restype = ctypes.c_uint64
         _lib = lib
     return _lib
 
@@ -153,3 +158,25 @@ def tags(ts, src, dst, nets, lens, start: int, window: int) -> np.ndarray:
                     len(ts), _ptr(nets, ctypes.c_uint32), _ptr(lens, ctypes.c_uint8), len(nets),
                     start, window, _ptr(out, ctypes.c_uint8))
     return out
+
+
+def rebin(fine, factor: int) -> np.ndarray:
+    """NEXT-1: coarse[k] = sum of fine[k*factor:(k+1)*factor] (u64, wraps)."""
+    fine = np.ascontiguousarray(fine, dtype=np.uint64)
+    out = np.zeros((len(fine) + factor - 1) // factor, dtype=np.uint64)
+    _load().oracle_rebin(_ptr(fine, ctypes.c_uint64), len(fine), factor, _ptr(out, ctypes.c_uint64))
+    return out
+
+
+def sparse(count, nbytes, start: int, width: int):
+    """NEXT-1: (bin start ms, count, bytes) of every nonzero-count bin, ascending."""
+    count = np.ascontiguousarray(count, dtype=np.uint64)
+    nbytes = np.ascontiguousarray(nbytes, dtype=np.uint64)
+    cap = int(np.count_nonzero(count))
+    t = np.zeros(cap, np.uint64)
+    c = np.zeros(cap, np.uint64)
+    b = np.zeros(cap, np.uint64)
+    k = _load().oracle_sparse(_ptr(count, ctypes.c_uint64), _ptr(nbytes, ctypes.c_uint64), len(count), start, width,
+                              _ptr(t, ctypes.c_uint64), _ptr(c, ctypes.c_uint64), _ptr(b, ctypes.c_uint64), cap)
+    assert k == cap
+    return t, c, b

@@ -201,3 +201,37 @@ int oracle_classify_histogram_mt(const uint64_t* ts, const uint32_t* src, const 
     free(jobs); free(tid);
     return rc;
 }
+
+/* ---------------------------------------------------------------------- */
+/* NEXT-1: re-binning and sparse export of one (dir, metric) plane.
+ * "Session data is grouped into one-hour frame bins" and counts
+ * "in 10 minutes": coarse bin k of a plane of fine bins is the sum
+ * of fine bins [k*factor, (k+1)*factor) (the last coarse bin may be partial).
+ * u64 sums wrap mod 2^64 (reading A18).                                     */
+void oracle_rebin(const uint64_t* fine, uint64_t nfine, uint64_t factor, uint64_t* coarse)
+{
+    uint64_t ncoarse = (nfine + factor - 1) / factor;
+    for (uint64_t k = 0; k < ncoarse; ++k) coarse[k] = 0;
+    for (uint64_t b = 0; b < nfine; ++b) coarse[b / factor] += fine[b];
+}
+
+/* Sparse series of one direction (the paper's key/value namespaces
+ * X1<timestamp>, X1<count>, X2<timestamp>, X2<bytes>):
+ * every bin with a nonzero count, ascending, as (bin start in epoch ms,
+ * count, bytes).  Returns the number of entries written (<= capacity).     */
+uint64_t oracle_sparse(const uint64_t* count, const uint64_t* bytes, uint64_t nbins,
+                       uint64_t start, uint32_t width,
+                       uint64_t* out_ts, uint64_t* out_count, uint64_t* out_bytes, uint64_t capacity)
+{
+    uint64_t k = 0;
+    for (uint64_t b = 0; b < nbins; ++b) {
+        if (count[b] == 0) continue;
+        if (k < capacity) {
+            out_ts[k] = start + b * (uint64_t)width;
+            out_count[k] = count[b];
+            out_bytes[k] = bytes[b];
+        }
+        ++k;
+    }
+    return k;
+}

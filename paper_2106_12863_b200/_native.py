@@ -67,6 +67,8 @@ _SIGS = {
     "sinet_owned_range": ([_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i),
     "sinet_read_bins": ([_vp, _i, _i, _u64, _u64, _vp, _i], _i),
     "sinet_read_totals": ([_vp, ctypes.POINTER(Totals)], _i),
+    "sinet_rebin": ([_vp, _u64, _vp, _u64], _i),
+    "sinet_export_sparse": ([_vp, _i, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i),
     "sinet_last_error": ([_vp], ctypes.c_char_p),
     "sinet_launch_count": ([_vp], _u64),
     "sinet_set_kernel_timing": ([_vp, _i], _i),

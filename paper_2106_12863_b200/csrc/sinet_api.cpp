@@ -90,7 +90,7 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, flags, total;
+    size_t totals, cls2, entry, bnd, flags, sparse, total;
 };
 
 WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
@@ -101,6 +101,7 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     L.entry = off;  off = align_up(off + 65536 * 4, 256);
     L.bnd = off;    off = align_up(off + ((size_t)2 * n_prefixes + 1) * 4, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
+    L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
     L.total = off;
     return L;
 }
@@ -529,6 +530,47 @@ int sinet_read_bins(sinet_ctx* c, int dir, int metric, uint64_t first, uint64_t 
     const unsigned long long* srcp = c->bins + (first * 4u + (uint64_t)dir * 2u + (uint64_t)metric);
     SINET_CUDA(c, cudaMemcpy2DAsync(dst, 8, srcp, 32, 8, n, dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
     if (!dst_is_device) SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SINET_OK;
+}
+
+int sinet_rebin(sinet_ctx* c, uint64_t factor, uint64_t* d_out, uint64_t n_out) {
+    if (!c) return SINET_E_INVAL;
+    if (factor == 0 || !d_out || (reinterpret_cast<uintptr_t>(d_out) & 7u))
+        return fail(c, SINET_E_INVAL, "rebin: factor must be >= 1 and d_out an 8-byte aligned device buffer");
+    uint64_t lo, cnt;
+    sinet_owned_range(c, &lo, &cnt);
+    if (n_out != (cnt + factor - 1) / factor) return fail(c, SINET_E_INVAL, "rebin: n_out must be ceil(owned bins / factor)");
+    DeviceGuard dg(c->device);
+    int rc = c->reduced ? SINET_OK : do_materialize(c);
+    if (rc) return rc;
+    SINET_CUDA(c, launch_rebin(c->bins, lo, lo + cnt, factor, reinterpret_cast<unsigned long long*>(d_out), n_out,
+                               c->sm_count, c->stream));
+    c->launches += (cnt ? 1 : 0);
+    return SINET_OK;
+}
+
+int sinet_export_sparse(sinet_ctx* c, int dir, uint64_t* d_ts, uint64_t* d_count, uint64_t* d_bytes,
+                        uint64_t capacity, uint64_t* n_nonzero) {
+    if (!c) return SINET_E_INVAL;
+    if (dir != SINET_DIR_OUT && dir != SINET_DIR_IN) return fail(c, SINET_E_INVAL, "dir must be SINET_DIR_OUT or SINET_DIR_IN");
+    if (!n_nonzero || (capacity && (!d_ts || !d_count || !d_bytes)))
+        return fail(c, SINET_E_INVAL, "export_sparse: NULL output");
+    uint64_t lo, cnt;
+    sinet_owned_range(c, &lo, &cnt);
+    DeviceGuard dg(c->device);
+    int rc = c->reduced ? SINET_OK : do_materialize(c);
+    if (rc) return rc;
+    unsigned long long* d_total = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.sparse);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(c->d_ws + c->ws.sparse + 16);
+    SINET_CUDA(c, launch_sparse(c->bins, lo, lo + cnt, (uint32_t)dir, scratch, d_total, c->cfg.window_start_ms,
+                                c->cfg.bin_width_ms, reinterpret_cast<unsigned long long*>(d_ts),
+                                reinterpret_cast<unsigned long long*>(d_count),
+                                reinterpret_cast<unsigned long long*>(d_bytes), capacity, c->stream));
+    c->launches += cnt ? (capacity ? 3 : 2) : 0;
+    unsigned long long h = 0;
+    SINET_CUDA(c, cudaMemcpyAsync(&h, d_total, 8, cudaMemcpyDeviceToHost, c->stream));
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    *n_nonzero = h;
     return SINET_OK;
 }
 

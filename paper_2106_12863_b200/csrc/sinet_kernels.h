@@ -20,4 +20,12 @@ cudaError_t setup_hist_stream();
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st);
 constexpr uint32_t kStreamWindowBins = 8192;
 
+cudaError_t launch_rebin(const unsigned long long* bins, uint64_t lo, uint64_t hi, uint64_t factor,
+                         unsigned long long* out, uint64_t n_out, int sm_count, cudaStream_t st);
+uint32_t sparse_blocks(uint64_t nbins);
+cudaError_t launch_sparse(const unsigned long long* bins, uint64_t lo, uint64_t hi, uint32_t dir, uint32_t* scratch,
+                          unsigned long long* d_total, uint64_t start, uint32_t width, unsigned long long* o_ts,
+                          unsigned long long* o_cnt, unsigned long long* o_bytes, uint64_t capacity,
+                          cudaStream_t st);
+
 }  // namespace sinet

@@ -186,6 +186,27 @@ class SinetHistogram:
               self.ctx, "read_bins")
         return out
 
+    def rebin(self, factor: int) -> torch.Tensor:
+        """Coarser frames of the owned range: int64[n_out, 2 dir, 2 metric] on the device (NEXT-1)."""
+        lo, hi = self.owned_range()
+        n_out = (hi - lo + factor - 1) // factor
+        out = torch.empty((max(n_out, 1), 2, 2), dtype=torch.int64, device=self.device)
+        check(lib.sinet_rebin(self.ctx, int(factor), _ptr(out), n_out), self.ctx, "rebin")
+        return out[:n_out]
+
+    def export_sparse(self, direction: int, capacity: int | None = None):
+        """(bin start ms, count, bytes) of every nonzero-count bin of `direction`, ascending (NEXT-1)."""
+        n = ctypes.c_uint64()
+        if capacity is None:
+            check(lib.sinet_export_sparse(self.ctx, direction, None, None, None, 0, ctypes.byref(n)),
+                  self.ctx, "export_sparse")
+            capacity = n.value
+        bufs = [torch.empty(max(capacity, 1), dtype=torch.int64, device=self.device) for _ in range(3)]
+        check(lib.sinet_export_sparse(self.ctx, direction, _ptr(bufs[0]), _ptr(bufs[1]), _ptr(bufs[2]), capacity,
+                                      ctypes.byref(n)), self.ctx, "export_sparse")
+        k = min(n.value, capacity)
+        return tuple(b[:k] for b in bufs), n.value
+
     def read_totals(self) -> np.ndarray:
         """12 x u64: m_count[4], m_bytes[4], oow_count[2], oow_bytes[2] (oracle layout)."""
         t = N.Totals()

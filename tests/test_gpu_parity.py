@@ -248,3 +248,34 @@ def test_c2_full_size_parity(S, oracle_lib, strategy):
         np.testing.assert_array_equal(h.read_bins(d, 0), o.count[d])
         np.testing.assert_array_equal(h.read_bins(d, 1), o.bytes[d])
     np.testing.assert_array_equal(h.read_totals(), o.totals)
+
+
+# ----------------------------------------------------------------------------- NEXT-1 series read-out
+@pytest.mark.parametrize("factor", [1, 7, 1000, 600_000, 3_600_000])
+def test_rebin_parity(S, oracle_lib, factor):
+    wl = WORKLOADS["c1"].with_(n=400_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms)
+    out = g["h"].rebin(factor).cpu().numpy().view(np.uint64)
+    for d in (0, 1):
+        np.testing.assert_array_equal(out[:, d, 0], oracle_lib.rebin(o.count[d], factor))
+        np.testing.assert_array_equal(out[:, d, 1], oracle_lib.rebin(o.bytes[d], factor))
+
+
+def test_sparse_export_parity(S, oracle_lib):
+    wl = WORKLOADS["c1"].with_(n=300_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms)
+    for d in (0, 1):
+        (t, c, b), n = g["h"].export_sparse(d)
+        et, ec, eb = oracle_lib.sparse(o.count[d], o.bytes[d], wl.window_start_ms, 1)
+        assert n == len(et)
+        np.testing.assert_array_equal(t.cpu().numpy().view(np.uint64), et)
+        np.testing.assert_array_equal(c.cpu().numpy().view(np.uint64), ec)
+        np.testing.assert_array_equal(b.cpu().numpy().view(np.uint64), eb)
+        (t2, _, _), n2 = g["h"].export_sparse(d, capacity=100)   # truncated output keeps the first entries
+        assert n2 == n and np.array_equal(t2.cpu().numpy().view(np.uint64), et[:100])

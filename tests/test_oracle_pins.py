@@ -281,3 +281,40 @@ def test_shuffled_generator_same_multiset(oracle_lib):
     sh = _run(oracle_lib, wl, nets, lens, to_numpy(rs))
     np.testing.assert_array_equal(sh.count, ref.count)
     np.testing.assert_array_equal(sh.bytes, ref.bytes)
+
+
+# ----------------------------------------------------------------------------- NEXT-1 rebin / sparse
+def test_rebin_worked_values_and_conservation(oracle_lib):
+    # (0,(1,10)) and (999,(1,20)) rebinned to 1000 ms -> [(0,(2,30))]
+    fine_c = np.zeros(2000, np.uint64)
+    fine_b = np.zeros(2000, np.uint64)
+    fine_c[[0, 999]] = 1
+    fine_b[[0, 999]] = [10, 20]
+    assert oracle_lib.rebin(fine_c, 1000).tolist() == [2, 0]
+    assert oracle_lib.rebin(fine_b, 1000).tolist() == [30, 0]
+    # 1 ms -> 10 min -> 1 h conserves totals and equals direct 1 h binning (S:L470 criterion 4)
+    wl, nets, lens, rec = _c1_small(100_000)
+    cols = to_numpy(rec)
+    fine = _run(oracle_lib, wl, nets, lens, cols)
+    hourly = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 3_600_000)
+    for d in (0, 1):
+        ten = oracle_lib.rebin(fine.count[d], 600_000)
+        assert int(ten.sum()) == int(fine.count[d].sum())
+        np.testing.assert_array_equal(oracle_lib.rebin(ten, 6), hourly.count[d])
+        np.testing.assert_array_equal(oracle_lib.rebin(fine.bytes[d], 3_600_000), hourly.bytes[d])
+    # partial last coarse bin, and u64 wrap
+    v = np.array([(1 << 64) - 1, 2, 5], np.uint64)
+    assert oracle_lib.rebin(v, 2).tolist() == [1, 5]
+
+
+def test_sparse_export_matches_definition(oracle_lib):
+    c = np.array([0, 3, 0, 0, 1, 0], np.uint64)
+    b = np.array([0, 30, 0, 0, 0, 0], np.uint64)
+    t, cc, bb = oracle_lib.sparse(c, b, 1000, 5)
+    assert t.tolist() == [1005, 1020] and cc.tolist() == [3, 1] and bb.tolist() == [30, 0]
+    wl, nets, lens, rec = _c1_small(50_000)
+    res = _run(oracle_lib, wl, nets, lens, to_numpy(rec))
+    t, cc, bb = oracle_lib.sparse(res.count[0], res.bytes[0], wl.window_start_ms, 1)
+    # sparse bound and conservation
+    assert len(t) <= min(wl.n, wl.nbins) and int(cc.sum()) == int(res.count[0].sum())
+    assert np.all(np.diff(t.astype(np.int64)) > 0)
