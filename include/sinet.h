@@ -159,6 +159,16 @@ int sinet_classify_histogram(sinet_ctx* ctx, const sinet_records* recs, uint8_t*
 int sinet_classify_histogram_host(sinet_ctx* ctx, const sinet_records* host_recs,
                                   void* d_staging, size_t staging_bytes, uint64_t chunk_records);
 
+/* NEXT-4 comparator -- the paper's own histogram design on this GPU:
+ * discriminate, emit <key = bin*2+dir, bytes> pairs, sort by key and
+ * reduce_by_key ("pairwise reduction"), then add each run into
+ * its bin.  Same semantics and result as sinet_classify_histogram (no tags);
+ * needs caller scratch of sinet_sortreduce_scratch_bytes(cfg, n) device bytes
+ * (~40 B/record).  n < 2^31 and 2B < 2^32.  Errors: as classify, E_INVAL. */
+size_t sinet_sortreduce_scratch_bytes(const sinet_config* cfg, uint64_t n);
+int sinet_classify_histogram_sortreduce(sinet_ctx* ctx, const sinet_records* recs,
+                                        void* d_scratch, size_t scratch_bytes);
+
 /* Materialise every bin (zero-fill tiles no record touched).  Idempotent;
  * called implicitly by sinet_reduce and sinet_read_bins. */
 int sinet_finalize(sinet_ctx* ctx);
@@ -222,7 +232,7 @@ uint64_t sinet_launch_count(const sinet_ctx* ctx);
  * number of timed launches since enabling (synchronises the stream). */
 int sinet_set_kernel_timing(sinet_ctx* ctx, int on);
 int sinet_kernel_time(sinet_ctx* ctx, double* total_ms, uint64_t* launches);
-/* Which accumulation strategy the last classify call used (SINET_ORDER_STREAM/SHUFFLED). */
+/* Which accumulation strategy the last classify call used (SINET_ORDER_STREAM/SHUFFLED, 3 = sort-reduce). */
 int sinet_last_strategy(const sinet_ctx* ctx);
 /* Host-side check of the prefix compiler (no GPU needed): compiles the CIDR
  * list exactly as sinet_open does and evaluates the same /16-class + boundary

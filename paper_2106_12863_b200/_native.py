@@ -68,6 +68,8 @@ _SIGS = {
     "sinet_read_bins": ([_vp, _i, _i, _u64, _u64, _vp, _i], _i),
     "sinet_read_totals": ([_vp, ctypes.POINTER(Totals)], _i),
     "sinet_rebin": ([_vp, _u64, _vp, _u64], _i),
+    "sinet_sortreduce_scratch_bytes": ([_CP, _u64], ctypes.c_size_t),
+    "sinet_classify_histogram_sortreduce": ([_vp, ctypes.POINTER(Records), _vp, ctypes.c_size_t], _i),
     "sinet_export_sparse": ([_vp, _i, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i),
     "sinet_last_error": ([_vp], ctypes.c_char_p),
     "sinet_launch_count": ([_vp], _u64),

@@ -228,19 +228,18 @@ int probe_order(sinet_ctx* c, const sinet_records* r, int* out) {
     return SINET_OK;
 }
 
-int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
+int prepare_params(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags, KernelParams* out) {
     if (c->reduced) return fail(c, SINET_E_STATE, "classify after reduce: call sinet_reset first");
     if (!r) return fail(c, SINET_E_INVAL, "NULL records");
-    if (r->n == 0) return SINET_OK;
     if (r->n > (1ull << 38)) return fail(c, SINET_E_INVAL, "batch larger than 2^38 records: split it");
-    if (!r->ts_ms || !r->src || !r->dst || !r->bytes) return fail(c, SINET_E_INVAL, "NULL record column");
+    if (r->n && (!r->ts_ms || !r->src || !r->dst || !r->bytes)) return fail(c, SINET_E_INVAL, "NULL record column");
     // Columns may start mid-way into a 16-byte group (e.g. a batch sliced at any
     // record index) as long as all four are offset by the same number of records.
     const uintptr_t a_ts = reinterpret_cast<uintptr_t>(r->ts_ms), a_src = reinterpret_cast<uintptr_t>(r->src),
                     a_dst = reinterpret_cast<uintptr_t>(r->dst), a_by = reinterpret_cast<uintptr_t>(r->bytes);
     const uint32_t head = (uint32_t)((a_src & 15u) >> 2);
-    if ((a_ts & 7u) || (a_by & 7u) || (a_src & 3u) || (a_dst & 3u) || ((a_dst & 15u) >> 2) != head ||
-        ((a_ts - 8u * head) & 15u) || ((a_by - 8u * head) & 15u))
+    if (r->n && ((a_ts & 7u) || (a_by & 7u) || (a_src & 3u) || (a_dst & 3u) || ((a_dst & 15u) >> 2) != head ||
+                 ((a_ts - 8u * head) & 15u) || ((a_by - 8u * head) & 15u)))
         return fail(c, SINET_E_ALIGN, "record columns must be naturally aligned and start at the same "
                                       "record offset within a 16-byte group (16-byte aligned bases)");
     KernelParams p = base_params(c);
@@ -248,7 +247,15 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
     p.head = head;
     p.nv = r->n + head;
     p.tags_vec = d_tags && (((reinterpret_cast<uintptr_t>(d_tags) - head) & 3u) == 0) ? 1u : 0u;
+    *out = p;
+    return SINET_OK;
+}
 
+int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
+    KernelParams p;
+    int prc = prepare_params(c, r, d_tags, &p);
+    if (prc) return prc;
+    if (r->n == 0) return SINET_OK;
     int strategy = (int)c->cfg.order_hint;
     if (strategy == SINET_ORDER_AUTO) {
         if (!c->auto_choice) {
@@ -443,6 +450,43 @@ int sinet_classify_histogram_host(sinet_ctx* c, const sinet_records* h, void* d_
         SINET_CUDA(c, cudaEventRecord(c->kern_done[b], c->stream));
     }
     SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SINET_OK;
+}
+
+size_t sinet_sortreduce_scratch_bytes(const sinet_config* cfg, uint64_t n) {
+    std::string err;
+    Geometry g;
+    if (!check_cfg(cfg, &err, &g) || n >= (1ull << 31) || g.B * 2 >= (1ull << 32)) return 0;
+    return sortreduce_scratch_bytes(n, g.B);
+}
+
+int sinet_classify_histogram_sortreduce(sinet_ctx* c, const sinet_records* r, void* d_scratch, size_t scratch_bytes) {
+    if (!c) return SINET_E_INVAL;
+    KernelParams p;
+    int prc = prepare_params(c, r, nullptr, &p);
+    if (prc) return prc;
+    if (r->n == 0) return SINET_OK;
+    if (r->n >= (1ull << 31) || c->geo.B * 2 >= (1ull << 32))
+        return fail(c, SINET_E_INVAL, "sort-reduce comparator: n < 2^31 and 2B < 2^32 required");
+    if (!d_scratch || scratch_bytes < sortreduce_scratch_bytes(r->n, c->geo.B))
+        return fail(c, SINET_E_INVAL, "sort-reduce comparator: scratch buffer too small");
+    DeviceGuard dg(c->device);
+    int rc = do_materialize(c);
+    if (rc) return rc;
+    int k = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        SINET_CUDA(c, cudaEventCreate(&e0));
+        SINET_CUDA(c, cudaEventCreate(&e1));
+        SINET_CUDA(c, cudaEventRecord(e0, c->stream));
+    }
+    SINET_CUDA(c, launch_sortreduce(p, d_scratch, scratch_bytes, c->sm_count, c->stream, &k));
+    if (c->timing) {
+        SINET_CUDA(c, cudaEventRecord(e1, c->stream));
+        c->tev.emplace_back(e0, e1);
+    }
+    c->launches += (uint64_t)k;
+    c->last_strategy = 3;
     return SINET_OK;
 }
 

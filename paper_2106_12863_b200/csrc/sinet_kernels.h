@@ -28,4 +28,8 @@ cudaError_t launch_sparse(const unsigned long long* bins, uint64_t lo, uint64_t 
                           unsigned long long* o_cnt, unsigned long long* o_bytes, uint64_t capacity,
                           cudaStream_t st);
 
+size_t sortreduce_scratch_bytes(uint64_t n, uint64_t nbins);
+cudaError_t launch_sortreduce(const KernelParams& p, void* scratch, size_t scratch_bytes, int sm_count,
+                              cudaStream_t st, int* launches);
+
 }  // namespace sinet

@@ -139,6 +139,16 @@ class SinetHistogram:
         check(lib.sinet_classify_histogram_host(self.ctx, ctypes.byref(recs), _ptr(self._staging), need,
                                                 chunk_records), self.ctx, "classify_host")
 
+    def classify_sortreduce(self, ts, src, dst, nbytes, scratch: torch.Tensor | None = None):
+        """NEXT-4 comparator: the paper's sort + reduce_by_key design (CUB), same result as classify()."""
+        recs = self._records(ts, src, dst, nbytes)
+        need = lib.sinet_sortreduce_scratch_bytes(ctypes.byref(self.cfg), recs.n)
+        if scratch is None or scratch.numel() < need:
+            scratch = torch.empty(max(need, 1), dtype=torch.uint8, device=self.device)
+        check(lib.sinet_classify_histogram_sortreduce(self.ctx, ctypes.byref(recs), _ptr(scratch), need),
+              self.ctx, "classify_sortreduce")
+        return scratch
+
     def finalize(self):
         check(lib.sinet_finalize(self.ctx), self.ctx, "finalize")
 

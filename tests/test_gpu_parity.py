@@ -279,3 +279,24 @@ def test_sparse_export_parity(S, oracle_lib):
         np.testing.assert_array_equal(b.cpu().numpy().view(np.uint64), eb)
         (t2, _, _), n2 = g["h"].export_sparse(d, capacity=100)   # truncated output keeps the first entries
         assert n2 == n and np.array_equal(t2.cpu().numpy().view(np.uint64), et[:100])
+
+
+# ----------------------------------------------------------------------------- NEXT-4 comparator
+@pytest.mark.parametrize("order", ["stream", "shuffled"])
+def test_sortreduce_comparator_parity(S, oracle_lib, order):
+    """The paper's sort + reduce_by_key design (CUB) gives the same bins as the oracle."""
+    wl = WORKLOADS["c1"].with_(order=order)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms)
+    d = dev_cols(cols)
+    scratch = h.classify_sortreduce(*d)
+    assert h.last_strategy == 3
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
+    # accumulates like classify(): a second pass doubles every bin
+    h.classify_sortreduce(*(c[1:] for c in d), scratch=scratch)
+    h.classify(*(c[:1] for c in d))
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count * np.uint64(2))
