@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--records-per-gpu", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-comparator", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
                     help="for ncu: no soak, no parity gate, no e2e, no CPU leg (numbers not valid)")
@@ -281,6 +282,11 @@ def run_ours(args):
     # ---- correctness gate (properties at full size + sampled bins vs the oracle)
     gate = None if args.profile else check_result(S, h, wl, ts, src, dst, nb, nets, lens, rank, world, dev)
 
+    # ---- NEXT-4 comparator: the paper's sort + reduce_by_key design on the same input
+    comp = None
+    if not args.no_comparator and not args.profile and world == 1:
+        comp = run_comparator(h, ts, src, dst, nb, args, wl)
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e and not args.profile:
@@ -323,6 +329,7 @@ def run_ours(args):
                               "note": "(24 B/record + 32 B/bin) per GPU / whole-step time"},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "comparator": comp,
             "gpu_launches": launches,
             "clocks": clk,
             "parity_gate": gate,
@@ -393,6 +400,37 @@ def check_result(S, h, wl, ts, src, dst, nb, nets, lens, rank, world, dev):
     if not ok:
         raise SystemExit("PARITY GATE FAILED: refusing to report a timing")
     return {"properties": True, "sampled_bins_vs_oracle": sampled}
+
+
+def run_comparator(h, ts, src, dst, nb, args, wl):
+    """The paper's histogram design (Thrust-style sort by key + reduce_by_key)
+    re-done with CUB on this GPU, same records, same C ABI semantics; bins must be identical."""
+    import torch
+    h.reset()
+    h.classify(ts, src, dst, nb)
+    h.reduce()
+    ref = h.bins_view()[: wl.nbins].clone()
+    ref_tot = h.read_totals()
+    scratch = None
+    k = max(1, min(args.steps, 5))
+    for i in range(2 + k):
+        if i == 2:
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        h.reset()
+        scratch = h.classify_sortreduce(ts, src, dst, nb, scratch=scratch)
+        h.reduce()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    same = bool(torch.equal(h.bins_view()[: wl.nbins], ref)) and np.array_equal(h.read_totals(), ref_tot)
+    del scratch, ref
+    torch.cuda.empty_cache()
+    return {"impl": "paper design on B200: classify -> cub radix sort by (bin,dir) -> reduce_by_key + "
+                    "run-length encode -> scatter (P:L213-214)", "ms_per_step": ms,
+            "value": wl.n / (ms * 1e-3), "unit": UNIT, "bins_identical": same}
 
 
 def run_e2e(h, ts, src, dst, nb, args, world, local, barrier):

@@ -52,39 +52,44 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
     return (uint64_t)a + ((uint64_t)b << 24) + ((uint64_t)c << 48);
 }
 
-struct WarpTotals {   // lane-uniform accumulators
-    uint64_t mc[4], mb[4], oc[2], ob[2];
+// Per-thread accumulators (predicated adds: ~16 thread-instructions per record,
+// half a warp-instruction per record), reduced once per CTA at the end.
+struct WarpTotals {
+    uint32_t mc[4], oc[2];
+    uint64_t mb[4], ob[2];
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { mc[k] = 0; mb[k] = 0; }
-        oc[0] = oc[1] = ob[0] = ob[1] = 0;
+        oc[0] = oc[1] = 0;
+        ob[0] = ob[1] = 0;
     }
-    // one record per lane (the whole warp must call it)
     __device__ __forceinline__ void add(bool valid, uint32_t cell, bool oow, uint32_t dir, uint64_t b) {
 #pragma unroll
-        for (uint32_t k = 0; k < 4; ++k) {
-            bool hit = valid && cell == k;
-            unsigned m = __ballot_sync(kFull, hit);
-            if (m) { mc[k] += (uint64_t)__popc(m); mb[k] += warp_sum_u64(hit ? b : 0ull); }
-        }
-#pragma unroll
-        for (uint32_t d = 0; d < 2; ++d) {
-            bool hit = oow && dir == d;
-            unsigned m = __ballot_sync(kFull, hit);
-            if (m) { oc[d] += (uint64_t)__popc(m); ob[d] += warp_sum_u64(hit ? b : 0ull); }
+        for (uint32_t k = 0; k < 4; ++k)
+            if (valid && cell == k) { mc[k] += 1u; mb[k] += b; }
+        if (oow) {
+            if (dir == 0u) { oc[0] += 1u; ob[0] += b; } else { oc[1] += 1u; ob[1] += b; }
         }
     }
 };
 
-// Sum the per-warp totals of a block and add them to the global totals (one RED per counter).
+// Sum the per-thread totals of a block and add them to the global totals (one RED per counter).
 __device__ __forceinline__ void flush_totals(const WarpTotals& t, unsigned long long* g_totals,
                                              unsigned long long* s_scratch /* [32][12] */) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (lane == 0) {
-        unsigned long long* s = s_scratch + warp * 12;
+    unsigned long long v[12];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { s[k] = t.mc[k]; s[4 + k] = t.mb[k]; }
-        s[8] = t.oc[0]; s[9] = t.oc[1]; s[10] = t.ob[0]; s[11] = t.ob[1];
+    for (int k = 0; k < 4; ++k) {
+        v[k] = __reduce_add_sync(kFull, t.mc[k]);
+        v[4 + k] = warp_sum_u64(t.mb[k]);
+    }
+    v[8] = __reduce_add_sync(kFull, t.oc[0]);
+    v[9] = __reduce_add_sync(kFull, t.oc[1]);
+    v[10] = warp_sum_u64(t.ob[0]);
+    v[11] = warp_sum_u64(t.ob[1]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 12; ++k) s_scratch[warp * 12 + k] = v[k];
     }
     __syncthreads();
     if (threadIdx.x < 12) {

@@ -26,6 +26,8 @@ namespace sinet {
 
 namespace {
 
+constexpr uint32_t kSpinLimit = 1u << 25;   // ~seconds of waiting on one tile: a protocol bug
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -41,11 +43,13 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 __device__ bool claim_or_wait(uint32_t* flag, uint32_t epoch) {
     const uint32_t claimed = (epoch << 2) | kTileClaimed, init = (epoch << 2) | kTileInit;
     uint32_t f = ld_acquire_u32(flag);
+    uint32_t spins = 0;
     for (;;) {
         if (f == init) return false;
         if (f == claimed) {
             __nanosleep(100);
             f = ld_acquire_u32(flag);
+            if (++spins > kSpinLimit) __trap();   // a protocol bug must fail loudly, not hang the GPU
             continue;
         }
         const uint32_t old = atomicCAS(flag, f, claimed);
@@ -75,31 +79,177 @@ __device__ void spill(const KernelParams& p, uint32_t bin, uint32_t dir, uint32_
 
 }  // namespace
 
-// Shared-memory window layout: 6 u32 per bin = {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in}.
+// Outcome of a tile claim, stored per ring slot tagged with the tile: (t+1) << 2 | outcome.
+constexpr uint32_t kWon = 1u;    // we initialise the tile: plain stores, then release
+constexpr uint32_t kInit = 2u;   // already initialised by someone else: add with RED
+constexpr uint32_t kBusy = 3u;   // claimed by someone else, not yet initialised: wait, then RED
+
+// One non-blocking claim attempt.  `old` is the value the first CAS returned
+// (expected = prev_word, the state most tiles are in); a tile still in an
+// older epoch is retried with the value seen.
+__device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch, uint32_t prev_word, uint32_t old) {
+    const uint32_t claimed = (epoch << 2) | kTileClaimed, init = (epoch << 2) | kTileInit;
+    uint32_t expect = prev_word;
+    for (;;) {
+        if (old == expect) return kWon;
+        if (old == init) return kInit;
+        if (old == claimed) return kBusy;
+        expect = old;
+        old = atomicCAS(flag, expect, claimed);
+    }
+}
+
+// Shared-memory window: a ring of NT tiles x 512 ms bins, 6 u32 per bin =
+// {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in}.  Tiles [lo_t, lo_t + NT)
+// are resident.  After a chunk is accumulated, tiles below the chunk's
+// oldest bin (keeping >= NT/2-1 tiles of history) are claimed with one
+// non-blocking CAS each; the CAS resolves while the next chunk is loaded and
+// classified, and the tiles are retired (stored or added) right after.  A CTA
+// never waits on another CTA's tile while it holds an unreleased claim, so
+// the protocol cannot deadlock.
 template <int THREADS, int WS, bool kBndSmem, bool kAgg>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     constexpr int NW = THREADS / 32;
-    constexpr uint32_t NTILE = WS / kTileBins;
+    constexpr uint32_t NT = WS / kTileBins;
     static_assert((WS & (WS - 1)) == 0 && WS % kTileBins == 0, "window must be a power of two of tiles");
-    static_assert((NTILE & (NTILE - 1)) == 0, "tiles per window must be a power of two");
+    static_assert(NT <= (uint32_t)THREADS && (NT & (NT - 1)) == 0, "tiles per window: power of two <= threads");
+    constexpr uint32_t kHist = NT / 2 - 1;   // tiles of history kept below a chunk's newest tile
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* s_win = smem;
     uint32_t* s_cls2 = s_win + WS * 6;
     __shared__ uint32_t s_red[2][2][NW];
-    __shared__ uint32_t s_touched[NTILE];
-    __shared__ uint32_t s_claim;
+    __shared__ uint32_t s_touched[NT];   // (t+1) of the tile last accumulated in this slot
+    __shared__ uint32_t s_state[NT];     // (t+1) << 2 | claim outcome
     __shared__ unsigned long long s_tot[NW * 12];
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t prev_word = p.epoch > 1 ? (((p.epoch - 1u) << 2) | kTileInit) : 0u;
     for (uint32_t i = tid; i < (uint32_t)WS * 6u / 4u; i += THREADS)
         reinterpret_cast<uint4*>(s_win)[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid < NTILE) s_touched[tid] = 0u;
+    if (tid < NT) { s_touched[tid] = 0u; s_state[tid] = 0u; }
     const uint32_t* bnd = stage_table(p, s_cls2, s_cls2 + kClsWords, kBndSmem);
     __syncthreads();
 
-    // accumulate (cnt, bytes) of one (bin, dir) into the window, or spill it
-    auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes, uint32_t wb) {
-        if (bin - wb < (uint32_t)WS) {
+    uint32_t lo_t = 0, act_t = 0;   // resident tiles [lo_t, lo_t+NT); [lo_t, act_t) claimed, to retire
+    bool have_window = false;
+    // this thread's in-flight claim (issued after a chunk, resolved before the next barrier)
+    uint32_t pend_t = 0xFFFFFFFFu, pend_old = 0u;
+
+    auto resolve_pending = [&]() {
+        if (pend_t != 0xFFFFFFFFu) {
+            const uint32_t o = claim_outcome(p.tile_flags + pend_t, p.epoch, prev_word, pend_old);
+            s_state[pend_t & (NT - 1)] = ((pend_t + 1u) << 2) | o;
+            pend_t = 0xFFFFFFFFu;
+        }
+    };
+    // thread k issues the claim CAS of tile t_from + k if it was touched (block-uniform call)
+    auto issue_claims = [&](uint32_t t_from, uint32_t t_to) {
+        if (tid < t_to - t_from) {
+            const uint32_t t = t_from + tid;
+            if (s_touched[t & (NT - 1)] == t + 1u) {
+                pend_t = t;
+                pend_old = atomicCAS(p.tile_flags + t, prev_word, (p.epoch << 2) | kTileClaimed);
+            }
+        }
+    };
+    // retire tiles [t_from, t_to) whose claims are resolved in s_state (block-uniform call;
+    // must be preceded by a barrier after the claims were resolved)
+    auto retire = [&](uint32_t t_from, uint32_t t_to) {
+        const uint32_t nt = t_to - t_from;
+        if (nt == 0) return;
+        bool busy = false;   // block-uniform: every thread evaluates the same s_state/s_touched
+        // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem
+        for (uint32_t k = 0; k < nt; ++k) {
+            const uint32_t t = t_from + k, slot = t & (NT - 1);
+            if (s_touched[slot] != t + 1u) continue;
+            const uint32_t st = s_state[slot];
+            const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
+            if (o == kBusy) { busy = true; continue; }
+            for (uint32_t i = tid; i < kTileBins; i += THREADS) {
+                const uint32_t bin = t * kTileBins + i;
+                uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
+                const uint2 c = *reinterpret_cast<const uint2*>(s);
+                const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
+                const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
+                const unsigned long long b_out = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
+                const unsigned long long b_in = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
+                if (o == kWon) {
+                    ulonglong2* g = reinterpret_cast<ulonglong2*>(p.bins + (size_t)bin * 4u);
+                    __stcg(g, make_ulonglong2(c.x, b_out));
+                    __stcg(g + 1, make_ulonglong2(c.y, b_in));
+                } else {
+                    unsigned long long* g64 = p.bins + (size_t)bin * 4u;
+                    if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (b_out) atomicAdd(g64 + 1, b_out); }
+                    if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y); if (b_in) atomicAdd(g64 + 3, b_in); }
+                }
+                *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
+                *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
+                *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
+            }
+        }
+        __syncthreads();
+        // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones
+        if (tid < nt) {
+            const uint32_t t = t_from + tid, slot = t & (NT - 1);
+            if (s_touched[slot] == t + 1u) {
+                const uint32_t st = s_state[slot];
+                const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
+                if (o == kWon) {
+                    __threadfence();
+                    st_release_u32(p.tile_flags + t, (p.epoch << 2) | kTileInit);
+                } else if (o == kBusy) {
+                    const uint32_t init = (p.epoch << 2) | kTileInit;
+                    uint32_t spins = 0;
+                    while (ld_acquire_u32(p.tile_flags + t) != init) {
+                        __nanosleep(200);
+                        if (++spins > kSpinLimit) __trap();
+                    }
+                }
+            }
+        }
+        if (busy) {
+            __syncthreads();
+            for (uint32_t k = 0; k < nt; ++k) {
+                const uint32_t t = t_from + k, slot = t & (NT - 1);
+                if (s_touched[slot] != t + 1u) continue;
+                const uint32_t st = s_state[slot];
+                if (((st >> 2) == t + 1u) && (st & 3u) != kBusy) continue;
+                for (uint32_t i = tid; i < kTileBins; i += THREADS) {
+                    const uint32_t bin = t * kTileBins + i;
+                    uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
+                    const uint2 c = *reinterpret_cast<const uint2*>(s);
+                    const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
+                    const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
+                    unsigned long long* g64 = p.bins + (size_t)bin * 4u;
+                    if (c.x) { atomicAdd(g64, (unsigned long long)c.x);
+                               const unsigned long long v = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
+                               if (v) atomicAdd(g64 + 1, v); }
+                    if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y);
+                               const unsigned long long v = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
+                               if (v) atomicAdd(g64 + 3, v); }
+                    *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
+                    *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
+                    *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
+                }
+            }
+            __syncthreads();
+        }
+    };
+    // claim synchronously (non-blocking CASes, resolved at once) and retire [t_from, t_to)
+    auto claim_and_retire = [&](uint32_t t_from, uint32_t t_to) {
+        for (uint32_t base = t_from; base < t_to; base += NT) {
+            const uint32_t e = (t_to - base < NT) ? t_to : base + NT;
+            issue_claims(base, e);
+            resolve_pending();
+            __syncthreads();
+            retire(base, e);
+        }
+    };
+
+    // accumulate (cnt, bytes) of one (bin, dir) into the ring, or spill it
+    auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) {
+        const uint32_t t = bin / kTileBins;
+        if (t - lo_t < NT) {
             uint32_t* s = s_win + (bin & (WS - 1)) * 6u + dir;
             atomicAdd(s, cnt);
             const uint32_t lo = (uint32_t)bytes;
@@ -107,47 +257,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t old = atomicAdd(s + 2, lo);
             hi += (old + lo < old) ? 1u : 0u;     // exact carry out of the low word
             if (hi) atomicAdd(s + 4, hi);
-            s_touched[(bin / kTileBins) & (NTILE - 1)] = 1u;
         } else {
             spill(p, bin, dir, cnt, bytes);
-        }
-    };
-
-    // retire tile t (absolute index) from the window to HBM; block-uniform call
-    auto flush_tile = [&](uint32_t t) {
-        const uint32_t slot_tile = t & (NTILE - 1);
-        if (!s_touched[slot_tile]) return;
-        if (tid == 0) s_claim = claim_or_wait(p.tile_flags + t, p.epoch) ? 1u : 0u;
-        __syncthreads();
-        const bool won = s_claim != 0u;
-        // every thread has read s_touched[slot_tile] above; clear it before the
-        // closing barrier so no accumulate of the next tile in this slot is lost
-        if (tid == 0) s_touched[slot_tile] = 0u;
-        for (uint32_t i = tid; i < kTileBins; i += THREADS) {
-            const uint32_t bin = t * kTileBins + i;
-            uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
-            const uint2 c = *reinterpret_cast<const uint2*>(s);
-            const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
-            const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
-            const unsigned long long b_out = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
-            const unsigned long long b_in = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
-            ulonglong2* g = reinterpret_cast<ulonglong2*>(p.bins + (size_t)bin * 4u);
-            if (won) {
-                __stcg(g, make_ulonglong2(c.x, b_out));
-                __stcg(g + 1, make_ulonglong2(c.y, b_in));
-            } else {
-                unsigned long long* g64 = p.bins + (size_t)bin * 4u;
-                if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (b_out) atomicAdd(g64 + 1, b_out); }
-                if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y); if (b_in) atomicAdd(g64 + 3, b_in); }
-            }
-            *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
-            *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
-            *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
-        }
-        __syncthreads();
-        if (tid == 0 && won) {
-            __threadfence();
-            st_release_u32(p.tile_flags + t, (p.epoch << 2) | kTileInit);
         }
     };
 
@@ -158,8 +269,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 
     WarpTotals tot;
     tot.zero();
-    uint32_t wb = 0;          // window base bin (multiple of kTileBins), block-uniform
-    bool have_window = false;
     Rec4 cur, nxt;
     if (g0 + tid < g1) load4(p, (g0 + tid) * 4, cur);
     uint32_t parity = 0;
@@ -169,6 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         const bool have = my_g < g1;
         if (cbase + THREADS + tid < g1) load4(p, (cbase + THREADS + tid) * 4, nxt);   // prefetch
 
+        // ---- a3-a5: classify and map this chunk (the claims issued last chunk resolve meanwhile)
         uint32_t bin4[4], dir4[4];
         bool binned4[4];
         uint32_t tag4 = 0, bmin = 0xFFFFFFFFu, bmax = 0u;
@@ -190,39 +300,56 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             tot.add(valid, cell, directed && !inw, dir, cur.by[j]);
         }
         if (p.tags && have) store_tags4(p, my_g * 4, tag4);
-
-        // block-wide extent of this chunk's bins
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
         if (lane == 0) { s_red[parity][0][warp] = bmin; s_red[parity][1][warp] = bmax; }
+        resolve_pending();
         __syncthreads();
         bmin = 0xFFFFFFFFu;
         bmax = 0u;
 #pragma unroll
         for (int w = 0; w < NW; ++w) { bmin = min(bmin, s_red[parity][0][w]); bmax = max(bmax, s_red[parity][1][w]); }
+        const bool any = bmin <= bmax;
+        const uint32_t bmin_t = bmin / kTileBins, bmax_t = bmax / kTileBins;
 
-        // slide the window so that it covers the chunk's newest bins
-        if (bmin <= bmax) {
+        // ---- a6 (retire): tiles claimed after the previous chunk
+        retire(lo_t, act_t);
+        lo_t = act_t;
+        if (any) {
             if (!have_window) {
-                wb = bmin & ~(kTileBins - 1u);
-                if (bmax - wb >= (uint32_t)WS) wb = (bmax + 1u - WS + kTileBins - 1u) & ~(kTileBins - 1u);
                 have_window = true;
-            } else if (bmax >= wb && bmax - wb >= (uint32_t)WS) {
-                const uint32_t nwb = (bmax + 1u - WS + kTileBins - 1u) & ~(kTileBins - 1u);
-                const uint32_t t0 = wb / kTileBins, nt = nwb / kTileBins - t0;
-                const uint32_t t1 = t0 + (nt < NTILE ? nt : NTILE);
-                for (uint32_t t = t0; t < t1; ++t) flush_tile(t);
-                wb = nwb;
+                lo_t = act_t = (bmax_t - bmin_t >= NT) ? bmax_t - NT + 1u : bmin_t;
+            } else if (bmax_t >= lo_t + NT) {   // the chunk reaches past the ring: retire now
+                const uint32_t nlo = bmax_t - NT + 1u;
+                claim_and_retire(lo_t, (nlo - lo_t < NT) ? nlo : lo_t + NT);
+                lo_t = act_t = nlo;
             }
         }
 
-        // Reduce the chunk into the window
+        // tiles of the ring this chunk reaches count as touched (block-uniform range)
+        if (any) {
+            const uint32_t ta = bmin_t > lo_t ? bmin_t : lo_t;
+            const uint32_t tb = bmax_t < lo_t + NT - 1u ? bmax_t : lo_t + NT - 1u;
+            if (ta <= tb && tid <= tb - ta) s_touched[(ta + tid) & (NT - 1)] = ta + tid + 1u;
+        }
+        // warp aggregation of equal (bin, dir) keys only where the chunk is denser
+        // than one record per bin (hot bins, bursts); block-uniform decision
+        const bool agg = kAgg && any && (bmax - bmin) < (uint32_t)(THREADS * 4);
+        const bool key32 = p.nbins < 0x40000000u;   // keys 2*bin+dir stay below the lane sentinels
+
+        // ---- a6 (accumulate): reduce the chunk into the ring
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool b = binned4[j];
-            if (kAgg) {
-                const unsigned long long key = b ? (((unsigned long long)bin4[j] << 1) | dir4[j]) : ~0ull - lane;
-                const unsigned m = __match_any_sync(kFull, key);
+            if (agg) {
+                unsigned m;
+                if (key32) {
+                    const uint32_t key = b ? ((bin4[j] << 1) | dir4[j]) : 0xFFFFFFFFu - lane;
+                    m = __match_any_sync(kFull, key);
+                } else {
+                    const unsigned long long key = b ? (((unsigned long long)bin4[j] << 1) | dir4[j]) : ~0ull - lane;
+                    m = __match_any_sync(kFull, key);
+                }
                 const bool big = __popc(m) >= 3;
                 if (__any_sync(kFull, big && b)) {
                     unsigned leaders = __ballot_sync(kFull, big && b && lane == (unsigned)(__ffs(m) - 1));
@@ -230,22 +357,36 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                         const int l = __ffs(leaders) - 1;
                         leaders &= leaders - 1;
                         const unsigned g = __shfl_sync(kFull, m, l);
-                        const uint64_t s = warp_sum_u64(((g >> lane) & 1u) ? cur.by[j] : 0ull);
-                        if (lane == (unsigned)l) accumulate(bin4[j], dir4[j], (uint32_t)__popc(g), s, wb);
+                        const uint64_t sum = warp_sum_u64(((g >> lane) & 1u) ? cur.by[j] : 0ull);
+                        if (lane == (unsigned)l) accumulate(bin4[j], dir4[j], (uint32_t)__popc(g), sum);
                     }
-                    if (b && !big) accumulate(bin4[j], dir4[j], 1u, cur.by[j], wb);
+                    if (b && !big) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
                     continue;
                 }
             }
-            if (b) accumulate(bin4[j], dir4[j], 1u, cur.by[j], wb);
+            if (b) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
         }
         cur = nxt;
+        __syncthreads();
+
+        // ---- claim the tiles that fall out of the history kept below this chunk
+        if (any) {
+            const uint32_t keep = (bmax_t >= kHist) ? bmax_t - kHist : 0u;
+            uint32_t nact = bmin_t < keep ? bmin_t : keep;
+            if (nact < act_t) nact = act_t;
+            if (nact > lo_t + NT) nact = lo_t + NT;
+            issue_claims(act_t, nact);
+            act_t = nact;
+        }
     }
 
-    // retire what is left in the window
+    // retire everything still resident
+    resolve_pending();
     __syncthreads();
-    if (have_window)
-        for (uint32_t t = wb / kTileBins, k = 0; k < NTILE; ++t, ++k) flush_tile(t);
+    if (have_window) {
+        retire(lo_t, act_t);
+        claim_and_retire(act_t, lo_t + NT);
+    }
     flush_totals(tot, p.totals, s_tot);
 }
 
