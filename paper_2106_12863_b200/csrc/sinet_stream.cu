@@ -58,23 +58,43 @@ __device__ bool claim_or_wait(uint32_t* flag, uint32_t epoch) {
     }
 }
 
-// One thread makes sure tile t is initialised (zero-filling it alone if it wins).
-__device__ void ensure_tile_single(const KernelParams& p, uint32_t t) {
-    uint32_t* flag = p.tile_flags + t;
-    if (claim_or_wait(flag, p.epoch)) {
-        ulonglong2* b = reinterpret_cast<ulonglong2*>(p.bins + (size_t)t * kTileBins * 4u);
-        const ulonglong2 z = make_ulonglong2(0ull, 0ull);
-        for (uint32_t i = 0; i < kTileBins * 2u; ++i) b[i] = z;
-        __threadfence();
-        st_release_u32(flag, (p.epoch << 2) | kTileInit);
+// Warp-cooperative spill (warp-uniform call): every lane with `need` adds
+// (cnt, bytes) to (bin, dir) in HBM.  For each distinct tile one lane claims
+// it (or waits until it is initialised); if it wins, the whole warp zero-fills
+// the tile and the lane publishes it.  No lane ever waits on a lane of its own
+// warp (a spin on a sibling lane could deadlock at the compiler's
+// reconvergence point), only on other warps/CTAs, which never wait while
+// holding a claim.
+__device__ void spill_warp(const KernelParams& p, bool need, uint32_t bin, uint32_t dir, uint32_t cnt,
+                           uint64_t bytes) {
+    const uint32_t lane = threadIdx.x & 31u;
+    unsigned pending = __ballot_sync(kFull, need);
+    const uint32_t t = bin / kTileBins;
+    while (pending) {
+        const int l = __ffs(pending) - 1;
+        const uint32_t tl = __shfl_sync(kFull, t, l);
+        uint32_t won = 0;
+        if (lane == 0) won = claim_or_wait(p.tile_flags + tl, p.epoch) ? 1u : 0u;
+        won = __shfl_sync(kFull, won, 0);
+        if (won) {
+            ulonglong2* b = reinterpret_cast<ulonglong2*>(p.bins + (size_t)tl * kTileBins * 4u);
+            const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+            for (uint32_t i = lane; i < kTileBins * 2u; i += 32u) b[i] = z;
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                st_release_u32(p.tile_flags + tl, (p.epoch << 2) | kTileInit);
+            }
+        }
+        __syncwarp();
+        const bool mine = need && t == tl;
+        if (mine) {
+            unsigned long long* slot = p.bins + ((size_t)bin * 4u + dir * 2u);
+            atomicAdd(slot, (unsigned long long)cnt);
+            if (bytes) atomicAdd(slot + 1, (unsigned long long)bytes);
+        }
+        pending &= ~__ballot_sync(kFull, mine);
     }
-}
-
-__device__ void spill(const KernelParams& p, uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) {
-    ensure_tile_single(p, bin / kTileBins);
-    unsigned long long* slot = p.bins + ((size_t)bin * 4u + dir * 2u);
-    atomicAdd(slot, (unsigned long long)cnt);
-    if (bytes) atomicAdd(slot + 1, (unsigned long long)bytes);
 }
 
 }  // namespace
@@ -246,20 +266,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         }
     };
 
-    // accumulate (cnt, bytes) of one (bin, dir) into the ring, or spill it
+    // accumulate (cnt, bytes) of one (bin, dir) into the ring (caller checked residency)
     auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) {
-        const uint32_t t = bin / kTileBins;
-        if (t - lo_t < NT) {
-            uint32_t* s = s_win + (bin & (WS - 1)) * 6u + dir;
-            atomicAdd(s, cnt);
-            const uint32_t lo = (uint32_t)bytes;
-            uint32_t hi = (uint32_t)(bytes >> 32);
-            const uint32_t old = atomicAdd(s + 2, lo);
-            hi += (old + lo < old) ? 1u : 0u;     // exact carry out of the low word
-            if (hi) atomicAdd(s + 4, hi);
-        } else {
-            spill(p, bin, dir, cnt, bytes);
-        }
+        uint32_t* s = s_win + (bin & (WS - 1)) * 6u + dir;
+        atomicAdd(s, cnt);
+        const uint32_t lo = (uint32_t)bytes;
+        uint32_t hi = (uint32_t)(bytes >> 32);
+        const uint32_t old = atomicAdd(s + 2, lo);
+        hi += (old + lo < old) ? 1u : 0u;     // exact carry out of the low word
+        if (hi) atomicAdd(s + 4, hi);
     };
 
     // this CTA's contiguous range of 4-record groups (virtual index space)
@@ -341,6 +356,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool b = binned4[j];
+            bool act = b;
+            uint32_t cnt = 1u;
+            uint64_t byt = cur.by[j];
             if (agg) {
                 unsigned m;
                 if (key32) {
@@ -350,21 +368,23 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                     const unsigned long long key = b ? (((unsigned long long)bin4[j] << 1) | dir4[j]) : ~0ull - lane;
                     m = __match_any_sync(kFull, key);
                 }
-                const bool big = __popc(m) >= 3;
-                if (__any_sync(kFull, big && b)) {
-                    unsigned leaders = __ballot_sync(kFull, big && b && lane == (unsigned)(__ffs(m) - 1));
+                const bool grouped = b && __popc(m) > 1;
+                if (__any_sync(kFull, grouped)) {
+                    const bool leader = lane == (unsigned)(__ffs(m) - 1);
+                    unsigned leaders = __ballot_sync(kFull, grouped && leader);
                     while (leaders) {
                         const int l = __ffs(leaders) - 1;
                         leaders &= leaders - 1;
                         const unsigned g = __shfl_sync(kFull, m, l);
                         const uint64_t sum = warp_sum_u64(((g >> lane) & 1u) ? cur.by[j] : 0ull);
-                        if (lane == (unsigned)l) accumulate(bin4[j], dir4[j], (uint32_t)__popc(g), sum);
+                        if (lane == (unsigned)l) { byt = sum; cnt = (uint32_t)__popc(g); }
                     }
-                    if (b && !big) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
-                    continue;
+                    act = b && (!grouped || leader);
                 }
             }
-            if (b) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
+            const bool in_ring = act && (bin4[j] / kTileBins - lo_t < NT);
+            if (in_ring) accumulate(bin4[j], dir4[j], cnt, byt);
+            spill_warp(p, act && !in_ring, bin4[j], dir4[j], cnt, byt);
         }
         cur = nxt;
         __syncthreads();

@@ -4,10 +4,10 @@ python -c "import paper_2106_12863_b200" || exit 1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -v -x --timeout 240 -k "not c2_full" > gpurun_out/pytest_gpu.txt 2>&1
 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-comparator > gpurun_out/bench_quick.txt 2>&1
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-comparator --strategy shuffled > gpurun_out/bench_shufstrat.txt 2>&1
 SINET_AGG=0 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-comparator > gpurun_out/bench_noagg.txt 2>&1
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-comparator --config c4 --records-per-gpu 400000000 > gpurun_out/bench_c4_400m.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o gpurun_out/prof_stream2 python bench.py --steps 2 --warmup 1 --profile > gpurun_out/ncu_full_run.txt 2>&1
+timeout 600 compute-sanitizer --tool memcheck python tools/sanitize_case.py > gpurun_out/san_memcheck.txt 2>&1
+timeout 900 compute-sanitizer --tool racecheck python tools/sanitize_case.py > gpurun_out/san_racecheck.txt 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full.txt 2>&1
-timeout 600 python -m pytest tests -m gpu -v -x --timeout 500 -k "c2_full" > gpurun_out/pytest_c2.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --profile > gpurun_out/ncu_launch_run.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o gpurun_out/prof_stream python bench.py --steps 2 --warmup 1 --profile > gpurun_out/ncu_full_run.txt 2>&1
 tail -n 3 gpurun_out/*.txt
