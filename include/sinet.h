@@ -177,7 +177,8 @@ int sinet_finalize(sinet_ctx* ctx);
 /* Build this rank's NCCL communicator from a 128-byte ncclUniqueId created by
  * rank 0 and shared by the caller (e.g. through torch.distributed).  NCCL is
  * loaded at run time (the libnccl.so.2 already in the process, else by name).
- * Errors: E_NCCL, E_INVAL (world == 1 needs no comm). */
+ * Optional with world == 1 (sinet_reduce then runs the same NCCL calls on a
+ * one-rank communicator).  Errors: E_NCCL, E_INVAL, E_STATE (already initialised). */
 int sinet_comm_init(sinet_ctx* ctx, const void* nccl_unique_id);
 
 /* Create a fresh 128-byte ncclUniqueId (rank 0), to be shared with the other
@@ -187,7 +188,7 @@ int sinet_nccl_unique_id(void* out128);
 /* Merge the per-GPU partial histograms (merge-scatter): finalize,
  * then an in-place reduce-scatter (u64 sum) leaves rank g the global sums of
  * bins [g*B_pad/world, (g+1)*B_pad/world); totals are all-reduced so every
- * rank holds the global totals.  world == 1: finalize only.
+ * rank holds the global totals.  world == 1 without a communicator: finalize only.
  * Errors: E_STATE (already reduced), E_NCCL (no comm / NCCL failure). */
 int sinet_reduce(sinet_ctx* ctx);
 

@@ -75,6 +75,17 @@ bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
         out->cls2[x >> 4] |= cls << ((x & 15u) * 2u);
         out->entry[x] = lo | (cnt << 16);
     }
+    out->hbits = 4;
+    while ((1u << out->hbits) < 2u * out->n_mixed) ++out->hbits;
+    out->hcap = 1u << out->hbits;
+    out->hash.assign(2u * out->hcap, 0u);
+    for (uint32_t x = 0; x < 65536; ++x) {
+        if (((out->cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u) != 2u) continue;
+        uint32_t h = (x * 0x9E3779B1u) >> (32u - out->hbits);
+        while (out->hash[2u * h] != 0u) h = (h + 1u) & (out->hcap - 1u);
+        out->hash[2u * h] = x + 1u;
+        out->hash[2u * h + 1u] = out->entry[x];
+    }
     return true;
 }
 

@@ -21,6 +21,10 @@ struct CompiledTable {
     std::vector<uint32_t> bnd;
     std::vector<uint32_t> cls2;
     std::vector<uint32_t> entry;
+    // open-addressing map of the mixed blocks: slot h = {x + 1, entry[x]} (0 = empty),
+    // home slot (x * 0x9E3779B1) >> (32 - hbits), linear probing; hcap = 2^hbits >= 2 * n_mixed
+    std::vector<uint32_t> hash;   // 2 * hcap u32 (uint2 pairs)
+    uint32_t hcap = 0, hbits = 0;
     uint32_t n_unique = 0;     // distinct normalised entries
     uint32_t n_intervals = 0;  // merged member intervals
     uint32_t n_mixed = 0;      // /16 blocks of class 2

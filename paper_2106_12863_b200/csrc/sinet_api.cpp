@@ -90,8 +90,15 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, flags, sparse, total;
+    size_t totals, cls2, entry, bnd, hash, flags, sparse, total;
 };
+
+// upper bound of the mixed-block hash capacity: n_mixed <= 2 * n_prefixes
+uint32_t hash_cap_bound(uint32_t n_prefixes) {
+    uint32_t bits = 4;
+    while ((1u << bits) < 4u * n_prefixes && bits < 17) ++bits;
+    return 1u << bits;
+}
 
 WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     WsLayout L{};
@@ -100,6 +107,7 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     L.cls2 = off;   off = align_up(off + (size_t)kClsWords * 4, 256);
     L.entry = off;  off = align_up(off + 65536 * 4, 256);
     L.bnd = off;    off = align_up(off + ((size_t)2 * n_prefixes + 1) * 4, 256);
+    L.hash = off;   off = align_up(off + (size_t)hash_cap_bound(n_prefixes) * 8, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
     L.total = off;
@@ -181,7 +189,11 @@ KernelParams base_params(sinet_ctx* c) {
     p.cls2 = ws_u32(c, c->ws.cls2);
     p.entry = ws_u32(c, c->ws.entry);
     p.bnd = ws_u32(c, c->ws.bnd);
+    p.hash = reinterpret_cast<const uint2*>(c->d_ws + c->ws.hash);
     p.nbnd = c->nbnd;
+    p.hcap = c->table.hcap;
+    p.hbits = c->table.hbits;
+    p.small = table_small(c->nbnd, c->table.hcap) ? 1u : 0u;
     p.lut = c->lut;
     p.start = c->cfg.window_start_ms;
     p.window = (uint32_t)c->cfg.window_ms;
@@ -357,7 +369,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     OPEN_CUDA(setup_hist_atomic());
     OPEN_CUDA(setup_hist_stream());
     if (const char* a = std::getenv("SINET_AGG")) c->agg = std::atoi(a) != 0;
-    c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(c->nbnd);
+    c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.totals, 0, 16 * 8, c->stream));
@@ -365,6 +377,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.entry, c->table.entry.data(), 65536 * 4, cudaMemcpyHostToDevice, c->stream));
     if (c->nbnd)
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.bnd, c->table.bnd.data(), (size_t)c->nbnd * 4, cudaMemcpyHostToDevice, c->stream));
+    OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.hash, c->table.hash.data(), c->table.hash.size() * 4, cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
     OPEN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
@@ -510,7 +523,6 @@ int sinet_nccl_unique_id(void* out) {
 
 int sinet_comm_init(sinet_ctx* c, const void* uid) {
     if (!c) return SINET_E_INVAL;
-    if (c->cfg.world == 1) return fail(c, SINET_E_INVAL, "world == 1 needs no communicator");
     if (!uid) return fail(c, SINET_E_INVAL, "NULL unique id");
     if (c->comm) return fail(c, SINET_E_STATE, "communicator already initialised");
     NcclApi* api = nccl_api(&c->err);
@@ -529,7 +541,7 @@ int sinet_reduce(sinet_ctx* c) {
     DeviceGuard dg(c->device);
     int rc = do_materialize(c);
     if (rc) return rc;
-    if (c->cfg.world > 1) {
+    if (c->cfg.world > 1 || c->comm) {
         if (!c->comm) return fail(c, SINET_E_NCCL, "no communicator: call sinet_comm_init");
         NcclApi* api = nccl_api(&c->err);
         if (!api) return SINET_E_NCCL;
@@ -641,7 +653,15 @@ int sinet_table_member_host(const uint32_t* net, const uint8_t* len, uint32_t np
         uint32_t ip = ips[i], x = ip >> 16;
         uint32_t c = (t.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
         if (c < 2u) { out[i] = (uint8_t)c; continue; }
-        uint32_t e = t.entry[x], cnt = e & 0xFFFFu, m = e >> 16;
+        // mixed block: the shared-memory hash the kernels probe (mixed_entry()), checked
+        // against the dense per-/16 table it was built from
+        uint32_t h = (x * 0x9E3779B1u) >> (32u - t.hbits);
+        while (t.hash[2u * h] != x + 1u) {
+            if (t.hash[2u * h] == 0u) return SINET_E_INVAL;   // compiler bug: mixed block missing
+            h = (h + 1u) & (t.hcap - 1u);
+        }
+        if (t.hash[2u * h + 1u] != t.entry[x]) return SINET_E_INVAL;
+        uint32_t e = t.hash[2u * h + 1u], cnt = e & 0xFFFFu, m = e >> 16;
         const uint32_t* b = t.bnd.data() + cnt;
         while (m) {
             uint32_t half = m >> 1;

@@ -9,19 +9,39 @@ namespace sinet {
 
 // ---------------------------------------------------------------- a3 + a4: membership
 // Alg. 1 l.6-9 against the compiled union of the CIDR list
-// (prefix_compile.cpp): one shared-memory load decides blocks wholly inside
-// or outside; mixed /16 blocks search their few boundaries.
-__device__ __forceinline__ uint32_t member(uint32_t ip, const uint32_t* s_cls2,
-                                           const uint32_t* __restrict__ entry,
-                                           const uint32_t* bnd) {
-    uint32_t x = ip >> 16;
-    uint32_t c = (s_cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
+// (prefix_compile.cpp): one shared-memory load decides /16 blocks wholly
+// inside or outside; a mixed block finds its boundary range in a small
+// shared-memory hash (or the global per-/16 table for big lists) and counts
+// the boundaries <= ip with a short binary search.
+struct Table {
+    const uint32_t* cls2;   // smem
+    const uint2* hash;      // smem, or nullptr -> use entry
+    const uint32_t* entry;  // global
+    const uint32_t* bnd;    // smem or global
+    uint32_t hbits, hmask;
+};
+
+__device__ __forceinline__ uint32_t mixed_entry(uint32_t x, const Table& T) {
+    if (T.hash) {
+        uint32_t h = (x * 0x9E3779B1u) >> (32u - T.hbits);
+        for (;;) {
+            const uint2 e = T.hash[h];
+            if (e.x == x + 1u) return e.y;
+            h = (h + 1u) & T.hmask;
+        }
+    }
+    return __ldg(T.entry + x);
+}
+
+__device__ __forceinline__ uint32_t member(uint32_t ip, const Table& T) {
+    const uint32_t x = ip >> 16;
+    const uint32_t c = (T.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
     if (c < 2u) return c;
-    uint32_t e = __ldg(entry + x);
+    const uint32_t e = mixed_entry(x, T);
     uint32_t cnt = e & 0xFFFFu, len = e >> 16;
-    const uint32_t* b = bnd + cnt;
+    const uint32_t* b = T.bnd + cnt;
     while (len) {
-        uint32_t half = len >> 1;
+        const uint32_t half = len >> 1;
         if (b[half] <= ip) { b += half + 1; cnt += half + 1; len -= half + 1; }
         else len = half;
     }
@@ -149,17 +169,30 @@ __device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t vbas
     }
 }
 
-// Stage the /16 class table (and small boundary arrays) into shared memory.
-__device__ __forceinline__ const uint32_t* stage_table(const KernelParams& p, uint32_t* s_cls2,
-                                                       uint32_t* s_bnd, bool bnd_in_smem) {
+// Stage the /16 class table (and, for small lists, the mixed-block hash and the
+// boundaries) into shared memory at `smem` (table_smem_bytes() bytes).
+__device__ __forceinline__ Table stage_table(const KernelParams& p, uint32_t* smem) {
+    Table T;
+    uint32_t* s_cls2 = smem;
     const uint4* g4 = reinterpret_cast<const uint4*>(p.cls2);
     uint4* s4 = reinterpret_cast<uint4*>(s_cls2);
     for (uint32_t i = threadIdx.x; i < kClsWords / 4; i += blockDim.x) s4[i] = __ldg(g4 + i);
-    if (bnd_in_smem) {
+    T.cls2 = s_cls2;
+    T.entry = p.entry;
+    T.hbits = p.hbits;
+    T.hmask = p.hcap - 1u;
+    if (p.small) {
+        uint2* s_hash = reinterpret_cast<uint2*>(smem + kClsWords);
+        uint32_t* s_bnd = smem + kClsWords + 2u * p.hcap;
+        for (uint32_t i = threadIdx.x; i < p.hcap; i += blockDim.x) s_hash[i] = p.hash[i];
         for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
-        return s_bnd;
+        T.hash = s_hash;
+        T.bnd = s_bnd;
+    } else {
+        T.hash = nullptr;
+        T.bnd = p.bnd;
     }
-    return p.bnd;
+    return T;
 }
 
 }  // namespace sinet

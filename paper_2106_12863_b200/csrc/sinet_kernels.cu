@@ -39,12 +39,10 @@ __global__ void __launch_bounds__(256) k_materialize(ulonglong2* bins, uint32_t*
 // Persistent grid; each warp takes 128 consecutive records per step (4 per
 // lane, vector loads), so the loop is warp-uniform and the totals can use
 // warp ballots/reductions.
-template <bool kBndSmem>
 __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_tot[32 * 12];
-    uint32_t* s_cls2 = smem;
-    const uint32_t* bnd = stage_table(p, s_cls2, smem + kClsWords, kBndSmem);
+    const Table T = stage_table(p, smem);
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -62,8 +60,8 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool valid = vvalid(p, base + j);
-            const uint32_t s_in = member(r.src[j], s_cls2, p.entry, bnd);
-            const uint32_t d_in = member(r.dst[j], s_cls2, p.entry, bnd);
+            const uint32_t s_in = member(r.src[j], T);
+            const uint32_t d_in = member(r.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
             const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
             uint32_t bin = 0;
@@ -93,31 +91,20 @@ cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32
     return cudaGetLastError();
 }
 
-size_t hist_atomic_smem(uint32_t nbnd) {
-    return (size_t)kClsWords * 4u + ((nbnd <= kMaxSmemBnd) ? (size_t)nbnd * 4u : 0u);
-}
-
 cudaError_t setup_hist_atomic() {
-    cudaError_t e = cudaFuncSetAttribute(k_hist_atomic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)hist_atomic_smem(kMaxSmemBnd));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_hist_atomic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)hist_atomic_smem(kMaxSmemBnd + 1));
+    return cudaFuncSetAttribute(k_hist_atomic, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)table_smem_bytes(kMaxSmemBnd, kMaxSmemHash, true));
 }
 
-int hist_atomic_blocks_per_sm(uint32_t nbnd) {
+int hist_atomic_blocks_per_sm(const KernelParams& p) {
     int nb = 0;
-    bool small = nbnd <= kMaxSmemBnd;
-    cudaError_t e = small
-        ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic<true>, 256, hist_atomic_smem(nbnd))
-        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic<false>, 256, hist_atomic_smem(nbnd));
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic, 256,
+                                                                  table_smem_bytes(p.nbnd, p.hcap, p.small));
     return (e == cudaSuccess && nb > 0) ? nb : 1;
 }
 
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st) {
-    size_t sm = hist_atomic_smem(p.nbnd);
-    if (p.nbnd <= kMaxSmemBnd) k_hist_atomic<true><<<grid, 256, sm, st>>>(p);
-    else k_hist_atomic<false><<<grid, 256, sm, st>>>(p);
+    k_hist_atomic<<<grid, 256, table_smem_bytes(p.nbnd, p.hcap, p.small), st>>>(p);
     return cudaGetLastError();
 }
 

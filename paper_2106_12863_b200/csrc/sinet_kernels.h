@@ -11,9 +11,8 @@ namespace sinet {
 cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32_t n_tiles,
                                uint32_t init_word, int grid, cudaStream_t st);
 
-size_t hist_atomic_smem(uint32_t nbnd);
 cudaError_t setup_hist_atomic();
-int hist_atomic_blocks_per_sm(uint32_t nbnd);
+int hist_atomic_blocks_per_sm(const KernelParams& p);
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st);
 
 cudaError_t setup_hist_stream();

@@ -1,12 +1,14 @@
 // Kernel parameter block and build constants shared by host launchers and device code.
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 
 namespace sinet {
 
 constexpr uint32_t kTileBins = 512;        // bins per claim tile (16 KB of u64[4] bins)
 constexpr uint32_t kClsWords = 4096;       // 65536 /16 blocks x 2 bits
 constexpr uint32_t kMaxSmemBnd = 4096;     // boundaries staged in shared memory up to this many
+constexpr uint32_t kMaxSmemHash = 1024;    // mixed-/16 hash slots staged in shared memory up to this many
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // tile state word: epoch << 2 | state
@@ -29,7 +31,11 @@ struct KernelParams {
     const uint32_t* cls2;          // [4096]
     const uint32_t* entry;         // [65536]
     const uint32_t* bnd;           // [nbnd]
+    const uint2* hash;             // [hcap] open-addressing map mixed /16 block x -> {x+1, entry}
     uint32_t nbnd;
+    uint32_t hcap;                 // power of two
+    uint32_t hbits;                // log2(hcap)
+    uint32_t small;                // 1: boundaries and hash fit in shared memory
     uint32_t lut;                  // 4 x 2 bits, index s_in*2+d_in
     uint64_t start;                // window start (ms)
     uint32_t window;               // W (ms) < 2^32
@@ -39,5 +45,11 @@ struct KernelParams {
     uint32_t epoch;                // current epoch
     uint32_t n_tiles;
 };
+
+// Shared-memory bytes of the staged lookup table: class table, hash, boundaries.
+inline unsigned long table_smem_bytes(uint32_t nbnd, uint32_t hcap, bool small) {
+    return (unsigned long)kClsWords * 4u + (small ? (unsigned long)hcap * 8u + (unsigned long)nbnd * 4u : 0u);
+}
+inline bool table_small(uint32_t nbnd, uint32_t hcap) { return nbnd <= kMaxSmemBnd && hcap <= kMaxSmemHash; }
 
 }  // namespace sinet

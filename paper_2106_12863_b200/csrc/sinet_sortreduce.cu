@@ -24,8 +24,7 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
                                                   unsigned long long* vals) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_tot[32 * 12];
-    uint32_t* s_cls2 = smem;
-    const uint32_t* bnd = stage_table(p, s_cls2, smem + kClsWords, p.nbnd <= kMaxSmemBnd);
+    const Table T = stage_table(p, smem);
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t wpb = blockDim.x >> 5;
@@ -40,8 +39,8 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool valid = vvalid(p, base + j);
-            const uint32_t s_in = member(r.src[j], s_cls2, p.entry, bnd);
-            const uint32_t d_in = member(r.dst[j], s_cls2, p.entry, bnd);
+            const uint32_t s_in = member(r.src[j], T);
+            const uint32_t d_in = member(r.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
             const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
             uint32_t bin = 0;
@@ -139,7 +138,7 @@ cudaError_t launch_sortreduce(const KernelParams& p, void* scratch, size_t scrat
     uint32_t* counts = reinterpret_cast<uint32_t*>(s + L.counts);
     int* nruns = reinterpret_cast<int*>(s + L.nruns);
     void* temp = s + L.temp;
-    const size_t smem = (size_t)kClsWords * 4u + ((p.nbnd <= kMaxSmemBnd) ? (size_t)p.nbnd * 4u : 0u);
+    const size_t smem = table_smem_bytes(p.nbnd, p.hcap, p.small);
     cudaError_t e = cudaFuncSetAttribute(k_map_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_map_keys<<<sm_count * 4, 256, smem, st>>>(p, sentinel, keys_in, vals_in);

@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
 // classified, and the tiles are retired (stored or added) right after.  A CTA
 // never waits on another CTA's tile while it holds an unreleased claim, so
 // the protocol cannot deadlock.
-template <int THREADS, int WS, bool kBndSmem, bool kAgg>
+template <int THREADS, int WS, bool kAgg>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     constexpr int NW = THREADS / 32;
     constexpr uint32_t NT = WS / kTileBins;
@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     constexpr uint32_t kHist = NT / 2 - 1;   // tiles of history kept below a chunk's newest tile
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* s_win = smem;
-    uint32_t* s_cls2 = s_win + WS * 6;
     __shared__ uint32_t s_red[2][2][NW];
     __shared__ uint32_t s_touched[NT];   // (t+1) of the tile last accumulated in this slot
     __shared__ uint32_t s_state[NT];     // (t+1) << 2 | claim outcome
@@ -147,7 +146,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     for (uint32_t i = tid; i < (uint32_t)WS * 6u / 4u; i += THREADS)
         reinterpret_cast<uint4*>(s_win)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (tid < NT) { s_touched[tid] = 0u; s_state[tid] = 0u; }
-    const uint32_t* bnd = stage_table(p, s_cls2, s_cls2 + kClsWords, kBndSmem);
+    const Table T = stage_table(p, s_win + WS * 6);
     __syncthreads();
 
     uint32_t lo_t = 0, act_t = 0;   // resident tiles [lo_t, lo_t+NT); [lo_t, act_t) claimed, to retire
@@ -300,8 +299,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool valid = have && vvalid(p, my_g * 4 + j);
-            const uint32_t s_in = member(cur.src[j], s_cls2, p.entry, bnd);
-            const uint32_t d_in = member(cur.dst[j], s_cls2, p.entry, bnd);
+            const uint32_t s_in = member(cur.src[j], T);
+            const uint32_t d_in = member(cur.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
             const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
             uint32_t bin = 0;
@@ -415,32 +414,27 @@ namespace {
 constexpr int kStreamThreads = 512;
 constexpr int kStreamWS = 8192;
 
-size_t stream_smem(uint32_t nbnd) {
-    return (size_t)kStreamWS * 6u * 4u + (size_t)kClsWords * 4u + ((nbnd <= kMaxSmemBnd) ? (size_t)nbnd * 4u : 0u);
+size_t stream_smem(const KernelParams& p) {
+    return (size_t)kStreamWS * 6u * 4u + table_smem_bytes(p.nbnd, p.hcap, p.small);
 }
 }  // namespace
 
 cudaError_t setup_hist_stream() {
-    cudaError_t e;
-#define SET(B, A)                                                                                   \
-    e = cudaFuncSetAttribute(k_hist_stream<kStreamThreads, kStreamWS, B, A>,                       \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(B ? kMaxSmemBnd : kMaxSmemBnd + 1)); \
+    const size_t mx = (size_t)kStreamWS * 6u * 4u + table_smem_bytes(kMaxSmemBnd, kMaxSmemHash, true);
+    cudaError_t e = cudaFuncSetAttribute(k_hist_stream<kStreamThreads, kStreamWS, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return e;
-    SET(true, true) SET(true, false) SET(false, true) SET(false, false)
-#undef SET
-    return cudaSuccess;
+    return cudaFuncSetAttribute(k_hist_stream<kStreamThreads, kStreamWS, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
 }
 
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st) {
-    const size_t sm = stream_smem(p.nbnd);
-    const bool small = p.nbnd <= kMaxSmemBnd;
+    const size_t sm = stream_smem(p);
     // one CTA per SM, but never more CTAs than chunks' worth of records
     uint64_t chunks = (p.nv / 4 + kStreamThreads - 1) / kStreamThreads;
     int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
-    if (small && agg) k_hist_stream<kStreamThreads, kStreamWS, true, true><<<grid, kStreamThreads, sm, st>>>(p);
-    else if (small) k_hist_stream<kStreamThreads, kStreamWS, true, false><<<grid, kStreamThreads, sm, st>>>(p);
-    else if (agg) k_hist_stream<kStreamThreads, kStreamWS, false, true><<<grid, kStreamThreads, sm, st>>>(p);
-    else k_hist_stream<kStreamThreads, kStreamWS, false, false><<<grid, kStreamThreads, sm, st>>>(p);
+    if (agg) k_hist_stream<kStreamThreads, kStreamWS, true><<<grid, kStreamThreads, sm, st>>>(p);
+    else k_hist_stream<kStreamThreads, kStreamWS, false><<<grid, kStreamThreads, sm, st>>>(p);
     return cudaGetLastError();
 }
 

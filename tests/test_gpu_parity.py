@@ -300,3 +300,20 @@ def test_sortreduce_comparator_parity(S, oracle_lib, order):
     h.classify_sortreduce(*(c[1:] for c in d), scratch=scratch)
     h.classify(*(c[:1] for c in d))
     np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count * np.uint64(2))
+
+
+def test_nccl_reduce_single_rank(S, oracle_lib):
+    """The NCCL merge path (run-time loaded libnccl, in-place u64 reduce-scatter +
+    totals all-reduce) on a one-rank communicator: bins and totals unchanged."""
+    wl = WORKLOADS["c1"].with_(n=200_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    import torch.distributed  # noqa: F401  (loads torch's libnccl.so.2 into the process)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms)
+    h.comm_init(S.SinetHistogram.new_unique_id())
+    h.classify(*dev_cols(cols))
+    h.reduce()
+    assert h.owned_range() == (0, wl.nbins)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
