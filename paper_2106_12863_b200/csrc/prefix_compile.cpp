@@ -79,12 +79,27 @@ bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
     while ((1u << out->hbits) < 2u * out->n_mixed) ++out->hbits;
     out->hcap = 1u << out->hbits;
     out->hash.assign(2u * out->hcap, 0u);
+    out->l2.assign((size_t)out->n_mixed * 16u, 0u);
+    uint32_t m = 0;
     for (uint32_t x = 0; x < 65536; ++x) {
         if (((out->cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u) != 2u) continue;
         uint32_t h = (x * 0x9E3779B1u) >> (32u - out->hbits);
         while (out->hash[2u * h] != 0u) h = (h + 1u) & (out->hcap - 1u);
-        out->hash[2u * h] = x + 1u;
+        out->hash[2u * h] = (x + 1u) | (m << 17);
         out->hash[2u * h + 1u] = out->entry[x];
+        // /24 sub-blocks: the same uniform/mixed test one level down
+        const uint32_t lo = out->entry[x] & 0xFFFFu, len = out->entry[x] >> 16;
+        for (uint32_t y = 0; y < 256; ++y) {
+            const uint32_t a = (x << 16) | (y << 8), z = a | 0xFFu;
+            uint32_t le_a = lo, le_z = lo;   // #boundaries <= a, <= z
+            for (uint32_t i = lo; i < lo + len; ++i) {
+                if (b[i] <= a) ++le_a;
+                if (b[i] <= z) ++le_z;
+            }
+            const uint32_t c2 = (le_a == le_z) ? (le_a & 1u) : 2u;
+            out->l2[(size_t)m * 16u + (y >> 4)] |= c2 << ((y & 15u) * 2u);
+        }
+        ++m;
     }
     return true;
 }

@@ -21,9 +21,13 @@ struct CompiledTable {
     std::vector<uint32_t> bnd;
     std::vector<uint32_t> cls2;
     std::vector<uint32_t> entry;
-    // open-addressing map of the mixed blocks: slot h = {x + 1, entry[x]} (0 = empty),
-    // home slot (x * 0x9E3779B1) >> (32 - hbits), linear probing; hcap = 2^hbits >= 2 * n_mixed
+    // open-addressing map of the mixed blocks: slot h = {(x + 1) | m << 17, entry[x]} (0 = empty),
+    // m = index of the block among the mixed blocks (ascending x); home slot
+    // (x * 0x9E3779B1) >> (32 - hbits), linear probing; hcap = 2^hbits >= 2 * n_mixed
     std::vector<uint32_t> hash;   // 2 * hcap u32 (uint2 pairs)
+    // level 2: for mixed block m, the 2-bit class of each of its 256 /24 sub-blocks
+    // (0 out, 1 in, 2 mixed -> boundary search), 16 words per block
+    std::vector<uint32_t> l2;
     uint32_t hcap = 0, hbits = 0;
     uint32_t n_unique = 0;     // distinct normalised entries
     uint32_t n_intervals = 0;  // merged member intervals

@@ -15,29 +15,29 @@ namespace sinet {
 // the boundaries <= ip with a short binary search.
 struct Table {
     const uint32_t* cls2;   // smem
-    const uint2* hash;      // smem, or nullptr -> use entry
+    const uint2* hash;      // smem, or nullptr -> global entry table, no level 2
+    const uint32_t* l2;     // smem level-2 /24 classes (with hash)
     const uint32_t* entry;  // global
     const uint32_t* bnd;    // smem or global
     uint32_t hbits, hmask;
 };
 
-__device__ __forceinline__ uint32_t mixed_entry(uint32_t x, const Table& T) {
-    if (T.hash) {
-        uint32_t h = (x * 0x9E3779B1u) >> (32u - T.hbits);
-        for (;;) {
-            const uint2 e = T.hash[h];
-            if (e.x == x + 1u) return e.y;
-            h = (h + 1u) & T.hmask;
-        }
-    }
-    return __ldg(T.entry + x);
-}
-
 __device__ __forceinline__ uint32_t member(uint32_t ip, const Table& T) {
     const uint32_t x = ip >> 16;
     const uint32_t c = (T.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
     if (c < 2u) return c;
-    const uint32_t e = mixed_entry(x, T);
+    uint32_t e;
+    if (T.hash) {
+        uint32_t h = (x * 0x9E3779B1u) >> (32u - T.hbits);
+        uint2 s = T.hash[h];
+        while ((s.x & 0x1FFFFu) != x + 1u) { h = (h + 1u) & T.hmask; s = T.hash[h]; }
+        const uint32_t y = (ip >> 8) & 0xFFu;
+        const uint32_t c2 = (T.l2[(s.x >> 17) * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
+        if (c2 < 2u) return c2;
+        e = s.y;
+    } else {
+        e = __ldg(T.entry + x);
+    }
     uint32_t cnt = e & 0xFFFFu, len = e >> 16;
     const uint32_t* b = T.bnd + cnt;
     while (len) {
@@ -183,13 +183,17 @@ __device__ __forceinline__ Table stage_table(const KernelParams& p, uint32_t* sm
     T.hmask = p.hcap - 1u;
     if (p.small) {
         uint2* s_hash = reinterpret_cast<uint2*>(smem + kClsWords);
-        uint32_t* s_bnd = smem + kClsWords + 2u * p.hcap;
+        uint32_t* s_l2 = smem + kClsWords + 2u * p.hcap;
+        uint32_t* s_bnd = s_l2 + 16u * p.n_mixed;
         for (uint32_t i = threadIdx.x; i < p.hcap; i += blockDim.x) s_hash[i] = p.hash[i];
+        for (uint32_t i = threadIdx.x; i < 16u * p.n_mixed; i += blockDim.x) s_l2[i] = __ldg(p.l2 + i);
         for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
         T.hash = s_hash;
+        T.l2 = s_l2;
         T.bnd = s_bnd;
     } else {
         T.hash = nullptr;
+        T.l2 = nullptr;
         T.bnd = p.bnd;
     }
     return T;

@@ -7,8 +7,7 @@ namespace sinet {
 
 constexpr uint32_t kTileBins = 512;        // bins per claim tile (16 KB of u64[4] bins)
 constexpr uint32_t kClsWords = 4096;       // 65536 /16 blocks x 2 bits
-constexpr uint32_t kMaxSmemBnd = 4096;     // boundaries staged in shared memory up to this many
-constexpr uint32_t kMaxSmemHash = 1024;    // mixed-/16 hash slots staged in shared memory up to this many
+constexpr uint32_t kSmallTableBytes = 33 * 1024;   // staged table (beyond the class table) fits in smem
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // tile state word: epoch << 2 | state
@@ -31,8 +30,10 @@ struct KernelParams {
     const uint32_t* cls2;          // [4096]
     const uint32_t* entry;         // [65536]
     const uint32_t* bnd;           // [nbnd]
-    const uint2* hash;             // [hcap] open-addressing map mixed /16 block x -> {x+1, entry}
+    const uint2* hash;             // [hcap] open-addressing map mixed /16 block x -> {x+1 | m<<17, entry}
+    const uint32_t* l2;            // [n_mixed * 16] 2-bit /24 classes of the mixed /16 blocks
     uint32_t nbnd;
+    uint32_t n_mixed;
     uint32_t hcap;                 // power of two
     uint32_t hbits;                // log2(hcap)
     uint32_t small;                // 1: boundaries and hash fit in shared memory
@@ -46,10 +47,16 @@ struct KernelParams {
     uint32_t n_tiles;
 };
 
-// Shared-memory bytes of the staged lookup table: class table, hash, boundaries.
-inline unsigned long table_smem_bytes(uint32_t nbnd, uint32_t hcap, bool small) {
-    return (unsigned long)kClsWords * 4u + (small ? (unsigned long)hcap * 8u + (unsigned long)nbnd * 4u : 0u);
+// Shared-memory bytes of the staged lookup table: class table + (small lists) hash, level 2, boundaries.
+inline unsigned long table_extra_bytes(uint32_t nbnd, uint32_t hcap, uint32_t n_mixed) {
+    return (unsigned long)hcap * 8u + (unsigned long)n_mixed * 64u + (unsigned long)nbnd * 4u;
 }
-inline bool table_small(uint32_t nbnd, uint32_t hcap) { return nbnd <= kMaxSmemBnd && hcap <= kMaxSmemHash; }
+inline bool table_small(uint32_t nbnd, uint32_t hcap, uint32_t n_mixed) {
+    return (unsigned long)kClsWords * 4u + table_extra_bytes(nbnd, hcap, n_mixed) <= kSmallTableBytes;
+}
+inline unsigned long table_smem_bytes(uint32_t nbnd, uint32_t hcap, uint32_t n_mixed, bool small) {
+    return (unsigned long)kClsWords * 4u + (small ? table_extra_bytes(nbnd, hcap, n_mixed) : 0u);
+}
+constexpr unsigned long kMaxTableSmem = kSmallTableBytes;
 
 }  // namespace sinet

@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* s_win = smem;
     __shared__ uint32_t s_red[2][2][NW];
-    __shared__ uint32_t s_touched[NT];   // (t+1) of the tile last accumulated in this slot
     __shared__ uint32_t s_state[NT];     // (t+1) << 2 | claim outcome
     __shared__ unsigned long long s_tot[NW * 12];
 
@@ -145,12 +144,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     const uint32_t prev_word = p.epoch > 1 ? (((p.epoch - 1u) << 2) | kTileInit) : 0u;
     for (uint32_t i = tid; i < (uint32_t)WS * 6u / 4u; i += THREADS)
         reinterpret_cast<uint4*>(s_win)[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid < NT) { s_touched[tid] = 0u; s_state[tid] = 0u; }
+    if (tid < NT) s_state[tid] = 0u;
     const Table T = stage_table(p, s_win + WS * 6);
     __syncthreads();
 
     uint32_t lo_t = 0, act_t = 0;   // resident tiles [lo_t, lo_t+NT); [lo_t, act_t) claimed, to retire
     bool have_window = false;
+    // hull of the tiles this CTA's chunks reached (block-uniform registers): a resident
+    // tile inside it may hold data and is claimed + retired; outside it is empty
+    uint32_t hull_lo = 0xFFFFFFFFu, hull_hi = 0u;
+    auto touched = [&](uint32_t t) { return t >= hull_lo && t <= hull_hi; };
     // this thread's in-flight claim (issued after a chunk, resolved before the next barrier)
     uint32_t pend_t = 0xFFFFFFFFu, pend_old = 0u;
 
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     auto issue_claims = [&](uint32_t t_from, uint32_t t_to) {
         if (tid < t_to - t_from) {
             const uint32_t t = t_from + tid;
-            if (s_touched[t & (NT - 1)] == t + 1u) {
+            if (touched(t)) {
                 pend_t = t;
                 pend_old = atomicCAS(p.tile_flags + t, prev_word, (p.epoch << 2) | kTileClaimed);
             }
@@ -176,11 +179,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     auto retire = [&](uint32_t t_from, uint32_t t_to) {
         const uint32_t nt = t_to - t_from;
         if (nt == 0) return;
-        bool busy = false;   // block-uniform: every thread evaluates the same s_state/s_touched
+        bool busy = false;   // block-uniform: every thread evaluates the same s_state
+        // thread k caches the outcome of tile t_from + k now: after the barrier below,
+        // threads already in the next chunk may re-use the slot for a newer claim
+        uint32_t my_o = 0u;
+        if (tid < nt && touched(t_from + tid)) {
+            const uint32_t t = t_from + tid, st = s_state[t & (NT - 1)];
+            my_o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
+        }
         // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = t_from + k, slot = t & (NT - 1);
-            if (s_touched[slot] != t + 1u) continue;
+            if (!touched(t)) continue;
             const uint32_t st = s_state[slot];
             const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
             if (o == kBusy) { busy = true; continue; }
@@ -209,10 +219,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         __syncthreads();
         // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones
         if (tid < nt) {
-            const uint32_t t = t_from + tid, slot = t & (NT - 1);
-            if (s_touched[slot] == t + 1u) {
-                const uint32_t st = s_state[slot];
-                const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
+            const uint32_t t = t_from + tid;
+            if (my_o != 0u) {
+                const uint32_t o = my_o;
                 if (o == kWon) {
                     __threadfence();
                     st_release_u32(p.tile_flags + t, (p.epoch << 2) | kTileInit);
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             __syncthreads();
             for (uint32_t k = 0; k < nt; ++k) {
                 const uint32_t t = t_from + k, slot = t & (NT - 1);
-                if (s_touched[slot] != t + 1u) continue;
+                if (!touched(t)) continue;
                 const uint32_t st = s_state[slot];
                 if (((st >> 2) == t + 1u) && (st & 3u) != kBusy) continue;
                 for (uint32_t i = tid; i < kTileBins; i += THREADS) {
@@ -340,11 +349,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             }
         }
 
-        // tiles of the ring this chunk reaches count as touched (block-uniform range)
-        if (any) {
-            const uint32_t ta = bmin_t > lo_t ? bmin_t : lo_t;
-            const uint32_t tb = bmax_t < lo_t + NT - 1u ? bmax_t : lo_t + NT - 1u;
-            if (ta <= tb && tid <= tb - ta) s_touched[(ta + tid) & (NT - 1)] = ta + tid + 1u;
+        if (any) {   // every resident tile this chunk reaches joins the hull
+            hull_lo = min(hull_lo, bmin_t > lo_t ? bmin_t : lo_t);
+            hull_hi = max(hull_hi, bmax_t);
         }
         // warp aggregation of equal (bin, dir) keys only where the chunk is denser
         // than one record per bin (hot bins, bursts); block-uniform decision
@@ -386,7 +393,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             spill_warp(p, act && !in_ring, bin4[j], dir4[j], cnt, byt);
         }
         cur = nxt;
-        __syncthreads();
 
         // ---- claim the tiles that fall out of the history kept below this chunk
         if (any) {
@@ -415,12 +421,12 @@ constexpr int kStreamThreads = 512;
 constexpr int kStreamWS = 8192;
 
 size_t stream_smem(const KernelParams& p) {
-    return (size_t)kStreamWS * 6u * 4u + table_smem_bytes(p.nbnd, p.hcap, p.small);
+    return (size_t)kStreamWS * 6u * 4u + table_smem_bytes(p.nbnd, p.hcap, p.n_mixed, p.small);
 }
 }  // namespace
 
 cudaError_t setup_hist_stream() {
-    const size_t mx = (size_t)kStreamWS * 6u * 4u + table_smem_bytes(kMaxSmemBnd, kMaxSmemHash, true);
+    const size_t mx = (size_t)kStreamWS * 6u * 4u + kMaxTableSmem;
     cudaError_t e = cudaFuncSetAttribute(k_hist_stream<kStreamThreads, kStreamWS, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return e;
