@@ -75,18 +75,17 @@ bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
         out->cls2[x >> 4] |= cls << ((x & 15u) * 2u);
         out->entry[x] = lo | (cnt << 16);
     }
-    out->hbits = 4;
-    while ((1u << out->hbits) < 2u * out->n_mixed) ++out->hbits;
-    out->hcap = 1u << out->hbits;
-    out->hash.assign(2u * out->hcap, 0u);
+    out->rank.assign(2048, 0u);
+    out->mentry.clear();
     out->l2.assign((size_t)out->n_mixed * 16u, 0u);
     uint32_t m = 0;
     for (uint32_t x = 0; x < 65536; ++x) {
+        if ((x & 15u) == 0) {
+            const uint32_t w = x >> 4;
+            out->rank[w >> 1] |= (m & 0xFFFFu) << ((w & 1u) * 16u);
+        }
         if (((out->cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u) != 2u) continue;
-        uint32_t h = (x * 0x9E3779B1u) >> (32u - out->hbits);
-        while (out->hash[2u * h] != 0u) h = (h + 1u) & (out->hcap - 1u);
-        out->hash[2u * h] = (x + 1u) | (m << 17);
-        out->hash[2u * h + 1u] = out->entry[x];
+        out->mentry.push_back(out->entry[x]);
         // /24 sub-blocks: the same uniform/mixed test one level down
         const uint32_t lo = out->entry[x] & 0xFFFFu, len = out->entry[x] >> 16;
         for (uint32_t y = 0; y < 256; ++y) {

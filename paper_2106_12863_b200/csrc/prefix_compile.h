@@ -21,14 +21,13 @@ struct CompiledTable {
     std::vector<uint32_t> bnd;
     std::vector<uint32_t> cls2;
     std::vector<uint32_t> entry;
-    // open-addressing map of the mixed blocks: slot h = {(x + 1) | m << 17, entry[x]} (0 = empty),
-    // m = index of the block among the mixed blocks (ascending x); home slot
-    // (x * 0x9E3779B1) >> (32 - hbits), linear probing; hcap = 2^hbits >= 2 * n_mixed
-    std::vector<uint32_t> hash;   // 2 * hcap u32 (uint2 pairs)
-    // level 2: for mixed block m, the 2-bit class of each of its 256 /24 sub-blocks
-    // (0 out, 1 in, 2 mixed -> boundary search), 16 words per block
+    // mixed blocks, numbered m = 0.. in ascending x:
+    //   rank[w]   = number of mixed blocks in cls2 words [0, w) (u16 pairs packed in u32)
+    //   mentry[m] = entry[x] of mixed block m
+    //   l2[m*16..] = 2-bit classes of its 256 /24 sub-blocks (0 out, 1 in, 2 mixed -> search)
+    std::vector<uint32_t> rank;     // 2048 u32 = 4096 u16
+    std::vector<uint32_t> mentry;
     std::vector<uint32_t> l2;
-    uint32_t hcap = 0, hbits = 0;
     uint32_t n_unique = 0;     // distinct normalised entries
     uint32_t n_intervals = 0;  // merged member intervals
     uint32_t n_mixed = 0;      // /16 blocks of class 2

@@ -90,15 +90,8 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, hash, l2, flags, sparse, total;
+    size_t totals, cls2, entry, bnd, rank, mentry, l2, flags, sparse, total;
 };
-
-// upper bound of the mixed-block hash capacity: n_mixed <= 2 * n_prefixes
-uint32_t hash_cap_bound(uint32_t n_prefixes) {
-    uint32_t bits = 4;
-    while ((1u << bits) < 4u * n_prefixes && bits < 17) ++bits;
-    return 1u << bits;
-}
 
 WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     WsLayout L{};
@@ -107,7 +100,8 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     L.cls2 = off;   off = align_up(off + (size_t)kClsWords * 4, 256);
     L.entry = off;  off = align_up(off + 65536 * 4, 256);
     L.bnd = off;    off = align_up(off + ((size_t)2 * n_prefixes + 1) * 4, 256);
-    L.hash = off;   off = align_up(off + (size_t)hash_cap_bound(n_prefixes) * 8, 256);
+    L.rank = off;   off = align_up(off + (size_t)kRankWords * 4, 256);
+    L.mentry = off; off = align_up(off + (size_t)(2u * n_prefixes + 1u) * 4, 256);
     L.l2 = off;     off = align_up(off + (size_t)(2u * n_prefixes + 1u) * 64, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
@@ -190,13 +184,12 @@ KernelParams base_params(sinet_ctx* c) {
     p.cls2 = ws_u32(c, c->ws.cls2);
     p.entry = ws_u32(c, c->ws.entry);
     p.bnd = ws_u32(c, c->ws.bnd);
-    p.hash = reinterpret_cast<const uint2*>(c->d_ws + c->ws.hash);
+    p.rank = ws_u32(c, c->ws.rank);
+    p.mentry = ws_u32(c, c->ws.mentry);
     p.l2 = ws_u32(c, c->ws.l2);
     p.n_mixed = c->table.n_mixed;
     p.nbnd = c->nbnd;
-    p.hcap = c->table.hcap;
-    p.hbits = c->table.hbits;
-    p.small = table_small(c->nbnd, c->table.hcap, c->table.n_mixed) ? 1u : 0u;
+    p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
     p.lut = c->lut;
     p.start = c->cfg.window_start_ms;
     p.window = (uint32_t)c->cfg.window_ms;
@@ -380,7 +373,9 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.entry, c->table.entry.data(), 65536 * 4, cudaMemcpyHostToDevice, c->stream));
     if (c->nbnd)
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.bnd, c->table.bnd.data(), (size_t)c->nbnd * 4, cudaMemcpyHostToDevice, c->stream));
-    OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.hash, c->table.hash.data(), c->table.hash.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.rank, c->table.rank.data(), (size_t)kRankWords * 4, cudaMemcpyHostToDevice, c->stream));
+    if (!c->table.mentry.empty())
+        OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.mentry, c->table.mentry.data(), c->table.mentry.size() * 4, cudaMemcpyHostToDevice, c->stream));
     if (!c->table.l2.empty())
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.l2, c->table.l2.data(), c->table.l2.size() * 4, cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
@@ -658,18 +653,17 @@ int sinet_table_member_host(const uint32_t* net, const uint8_t* len, uint32_t np
         uint32_t ip = ips[i], x = ip >> 16;
         uint32_t c = (t.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
         if (c < 2u) { out[i] = (uint8_t)c; continue; }
-        // mixed block: the shared-memory hash + level-2 /24 classes the kernels probe
-        // (member() in sinet_device.cuh), checked against the dense per-/16 table
-        uint32_t h = (x * 0x9E3779B1u) >> (32u - t.hbits);
-        while ((t.hash[2u * h] & 0x1FFFFu) != x + 1u) {
-            if (t.hash[2u * h] == 0u) return SINET_E_INVAL;   // compiler bug: mixed block missing
-            h = (h + 1u) & (t.hcap - 1u);
-        }
-        if (t.hash[2u * h + 1u] != t.entry[x]) return SINET_E_INVAL;
-        const uint32_t y = (ip >> 8) & 0xFFu, mi = t.hash[2u * h] >> 17;
+        // mixed block: rank + level-2 /24 classes + per-block entry, exactly as the kernels'
+        // member() in sinet_device.cuh, with the dense per-/16 table as a cross-check
+        const uint32_t w = t.cls2[x >> 4], sh = (x & 15u) * 2u;
+        const uint32_t mixed = (w >> 1) & ~w & 0x55555555u;
+        const uint16_t* rk = reinterpret_cast<const uint16_t*>(t.rank.data());
+        const uint32_t mi = rk[x >> 4] + (uint32_t)__builtin_popcount(mixed & ((1u << sh) - 1u));
+        if (mi >= t.n_mixed || t.mentry[mi] != t.entry[x]) return SINET_E_INVAL;   // compiler bug
+        const uint32_t y = (ip >> 8) & 0xFFu;
         const uint32_t c2 = (t.l2[(size_t)mi * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
         if (c2 < 2u) { out[i] = (uint8_t)c2; continue; }
-        uint32_t e = t.hash[2u * h + 1u], cnt = e & 0xFFFFu, m = e >> 16;
+        uint32_t e = t.mentry[mi], cnt = e & 0xFFFFu, m = e >> 16;
         const uint32_t* b = t.bnd.data() + cnt;
         while (m) {
             uint32_t half = m >> 1;

@@ -10,34 +10,32 @@ namespace sinet {
 // ---------------------------------------------------------------- a3 + a4: membership
 // Alg. 1 l.6-9 against the compiled union of the CIDR list
 // (prefix_compile.cpp): one shared-memory load decides /16 blocks wholly
-// inside or outside; a mixed block finds its boundary range in a small
-// shared-memory hash (or the global per-/16 table for big lists) and counts
-// the boundaries <= ip with a short binary search.
+// inside or outside; a mixed block is resolved at /24 granularity by a level-2
+// class table, and only a mixed /24 counts its boundaries <= ip.
 struct Table {
-    const uint32_t* cls2;   // smem
-    const uint2* hash;      // smem, or nullptr -> global entry table, no level 2
-    const uint32_t* l2;     // smem level-2 /24 classes (with hash)
-    const uint32_t* entry;  // global
-    const uint32_t* bnd;    // smem or global
-    uint32_t hbits, hmask;
+    const uint32_t* cls2;    // smem
+    const uint16_t* rank;    // smem
+    const uint32_t* l2;      // smem (small lists) or global
+    const uint32_t* mentry;  // smem (small lists) or global
+    const uint32_t* bnd;     // smem (small lists) or global
 };
 
+// member(ip): 1 LDS for a /16 wholly in or out; a mixed /16 finds its index m among the
+// mixed blocks by rank (prefix count of the class-table word + popcount of the mixed
+// codes before it in the word already loaded), then 1 LDS of its /24 class; only a
+// mixed /24 (prefixes longer than /24) searches the block's few boundaries.
 __device__ __forceinline__ uint32_t member(uint32_t ip, const Table& T) {
     const uint32_t x = ip >> 16;
-    const uint32_t c = (T.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
+    const uint32_t w = T.cls2[x >> 4];
+    const uint32_t sh = (x & 15u) * 2u;
+    const uint32_t c = (w >> sh) & 3u;
     if (c < 2u) return c;
-    uint32_t e;
-    if (T.hash) {
-        uint32_t h = (x * 0x9E3779B1u) >> (32u - T.hbits);
-        uint2 s = T.hash[h];
-        while ((s.x & 0x1FFFFu) != x + 1u) { h = (h + 1u) & T.hmask; s = T.hash[h]; }
-        const uint32_t y = (ip >> 8) & 0xFFu;
-        const uint32_t c2 = (T.l2[(s.x >> 17) * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
-        if (c2 < 2u) return c2;
-        e = s.y;
-    } else {
-        e = __ldg(T.entry + x);
-    }
+    const uint32_t mixed = (w >> 1) & ~w & 0x55555555u;          // bit 2i: block i of the word is mixed
+    const uint32_t m = T.rank[x >> 4] + __popc(mixed & ((1u << sh) - 1u));
+    const uint32_t y = (ip >> 8) & 0xFFu;
+    const uint32_t c2 = (T.l2[m * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
+    if (c2 < 2u) return c2;
+    const uint32_t e = T.mentry[m];
     uint32_t cnt = e & 0xFFFFu, len = e >> 16;
     const uint32_t* b = T.bnd + cnt;
     while (len) {
@@ -169,31 +167,31 @@ __device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t vbas
     }
 }
 
-// Stage the /16 class table (and, for small lists, the mixed-block hash and the
-// boundaries) into shared memory at `smem` (table_smem_bytes() bytes).
+// Stage the /16 class table and the mixed-block rank (and, for small lists, the
+// level-2 classes, entries and boundaries) into shared memory at `smem`
+// (table_smem_bytes() bytes).
 __device__ __forceinline__ Table stage_table(const KernelParams& p, uint32_t* smem) {
     Table T;
-    uint32_t* s_cls2 = smem;
     const uint4* g4 = reinterpret_cast<const uint4*>(p.cls2);
-    uint4* s4 = reinterpret_cast<uint4*>(s_cls2);
+    uint4* s4 = reinterpret_cast<uint4*>(smem);
     for (uint32_t i = threadIdx.x; i < kClsWords / 4; i += blockDim.x) s4[i] = __ldg(g4 + i);
-    T.cls2 = s_cls2;
-    T.entry = p.entry;
-    T.hbits = p.hbits;
-    T.hmask = p.hcap - 1u;
+    uint32_t* s_rank = smem + kClsWords;
+    for (uint32_t i = threadIdx.x; i < kRankWords; i += blockDim.x) s_rank[i] = __ldg(p.rank + i);
+    T.cls2 = smem;
+    T.rank = reinterpret_cast<const uint16_t*>(s_rank);
     if (p.small) {
-        uint2* s_hash = reinterpret_cast<uint2*>(smem + kClsWords);
-        uint32_t* s_l2 = smem + kClsWords + 2u * p.hcap;
-        uint32_t* s_bnd = s_l2 + 16u * p.n_mixed;
-        for (uint32_t i = threadIdx.x; i < p.hcap; i += blockDim.x) s_hash[i] = p.hash[i];
+        uint32_t* s_l2 = s_rank + kRankWords;
+        uint32_t* s_me = s_l2 + 16u * p.n_mixed;
+        uint32_t* s_bnd = s_me + p.n_mixed;
         for (uint32_t i = threadIdx.x; i < 16u * p.n_mixed; i += blockDim.x) s_l2[i] = __ldg(p.l2 + i);
+        for (uint32_t i = threadIdx.x; i < p.n_mixed; i += blockDim.x) s_me[i] = __ldg(p.mentry + i);
         for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
-        T.hash = s_hash;
         T.l2 = s_l2;
+        T.mentry = s_me;
         T.bnd = s_bnd;
     } else {
-        T.hash = nullptr;
-        T.l2 = nullptr;
+        T.l2 = p.l2;
+        T.mentry = p.mentry;
         T.bnd = p.bnd;
     }
     return T;

@@ -99,12 +99,12 @@ cudaError_t setup_hist_atomic() {
 int hist_atomic_blocks_per_sm(const KernelParams& p) {
     int nb = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic, 256,
-                                                                  table_smem_bytes(p.nbnd, p.hcap, p.n_mixed, p.small));
+                                                                  table_smem_bytes(p.nbnd, p.n_mixed, p.small));
     return (e == cudaSuccess && nb > 0) ? nb : 1;
 }
 
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st) {
-    k_hist_atomic<<<grid, 256, table_smem_bytes(p.nbnd, p.hcap, p.n_mixed, p.small), st>>>(p);
+    k_hist_atomic<<<grid, 256, table_smem_bytes(p.nbnd, p.n_mixed, p.small), st>>>(p);
     return cudaGetLastError();
 }
 

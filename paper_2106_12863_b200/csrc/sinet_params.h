@@ -7,7 +7,9 @@ namespace sinet {
 
 constexpr uint32_t kTileBins = 512;        // bins per claim tile (16 KB of u64[4] bins)
 constexpr uint32_t kClsWords = 4096;       // 65536 /16 blocks x 2 bits
-constexpr uint32_t kSmallTableBytes = 33 * 1024;   // staged table (beyond the class table) fits in smem
+constexpr uint32_t kRankWords = 2048;      // 4096 u16 prefix counts
+// staged beyond the class table + rank (24 KB): level 2 + entries + boundaries if they fit here
+constexpr uint32_t kSmallExtraBytes = 9 * 1024;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // tile state word: epoch << 2 | state
@@ -30,13 +32,12 @@ struct KernelParams {
     const uint32_t* cls2;          // [4096]
     const uint32_t* entry;         // [65536]
     const uint32_t* bnd;           // [nbnd]
-    const uint2* hash;             // [hcap] open-addressing map mixed /16 block x -> {x+1 | m<<17, entry}
+    const uint32_t* rank;          // [2048] u16 pairs: mixed blocks before each class-table word
+    const uint32_t* mentry;        // [n_mixed] entry of each mixed /16 block
     const uint32_t* l2;            // [n_mixed * 16] 2-bit /24 classes of the mixed /16 blocks
     uint32_t nbnd;
     uint32_t n_mixed;
-    uint32_t hcap;                 // power of two
-    uint32_t hbits;                // log2(hcap)
-    uint32_t small;                // 1: boundaries and hash fit in shared memory
+    uint32_t small;                // 1: level 2, entries and boundaries fit in shared memory
     uint32_t lut;                  // 4 x 2 bits, index s_in*2+d_in
     uint64_t start;                // window start (ms)
     uint32_t window;               // W (ms) < 2^32
@@ -47,16 +48,15 @@ struct KernelParams {
     uint32_t n_tiles;
 };
 
-// Shared-memory bytes of the staged lookup table: class table + (small lists) hash, level 2, boundaries.
-inline unsigned long table_extra_bytes(uint32_t nbnd, uint32_t hcap, uint32_t n_mixed) {
-    return (unsigned long)hcap * 8u + (unsigned long)n_mixed * 64u + (unsigned long)nbnd * 4u;
+// Shared-memory bytes of the staged lookup table: class table + rank (+ small lists: level 2,
+// entries, boundaries).
+inline unsigned long table_extra_bytes(uint32_t nbnd, uint32_t n_mixed) {
+    return (unsigned long)n_mixed * 68u + (unsigned long)nbnd * 4u;
 }
-inline bool table_small(uint32_t nbnd, uint32_t hcap, uint32_t n_mixed) {
-    return (unsigned long)kClsWords * 4u + table_extra_bytes(nbnd, hcap, n_mixed) <= kSmallTableBytes;
+inline bool table_small(uint32_t nbnd, uint32_t n_mixed) { return table_extra_bytes(nbnd, n_mixed) <= kSmallExtraBytes; }
+inline unsigned long table_smem_bytes(uint32_t nbnd, uint32_t n_mixed, bool small) {
+    return (unsigned long)(kClsWords + kRankWords) * 4u + (small ? table_extra_bytes(nbnd, n_mixed) : 0u);
 }
-inline unsigned long table_smem_bytes(uint32_t nbnd, uint32_t hcap, uint32_t n_mixed, bool small) {
-    return (unsigned long)kClsWords * 4u + (small ? table_extra_bytes(nbnd, hcap, n_mixed) : 0u);
-}
-constexpr unsigned long kMaxTableSmem = kSmallTableBytes;
+constexpr unsigned long kMaxTableSmem = (unsigned long)(kClsWords + kRankWords) * 4u + kSmallExtraBytes;
 
 }  // namespace sinet

@@ -138,7 +138,7 @@ cudaError_t launch_sortreduce(const KernelParams& p, void* scratch, size_t scrat
     uint32_t* counts = reinterpret_cast<uint32_t*>(s + L.counts);
     int* nruns = reinterpret_cast<int*>(s + L.nruns);
     void* temp = s + L.temp;
-    const size_t smem = table_smem_bytes(p.nbnd, p.hcap, p.n_mixed, p.small);
+    const size_t smem = table_smem_bytes(p.nbnd, p.n_mixed, p.small);
     cudaError_t e = cudaFuncSetAttribute(k_map_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_map_keys<<<sm_count * 4, 256, smem, st>>>(p, sentinel, keys_in, vals_in);

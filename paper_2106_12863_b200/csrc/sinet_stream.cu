@@ -421,7 +421,7 @@ constexpr int kStreamThreads = 512;
 constexpr int kStreamWS = 8192;
 
 size_t stream_smem(const KernelParams& p) {
-    return (size_t)kStreamWS * 6u * 4u + table_smem_bytes(p.nbnd, p.hcap, p.n_mixed, p.small);
+    return (size_t)kStreamWS * 6u * 4u + table_smem_bytes(p.nbnd, p.n_mixed, p.small);
 }
 }  // namespace
 
