@@ -231,8 +231,8 @@ int probe_order(sinet_ctx* c, const sinet_records* r, int* out) {
         span[k] = hi - lo;
     }
     std::nth_element(span.begin(), span.begin() + kRuns / 2, span.end());
-    const uint64_t limit = (uint64_t)kStreamWindowBins / 2 * c->cfg.bin_width_ms;
-    *out = (span[kRuns / 2] <= limit) ? SINET_ORDER_STREAM : SINET_ORDER_SHUFFLED;
+    const uint64_t limit = (uint64_t)kStreamWindowBins * c->cfg.bin_width_ms;
+    *out = (span[kRuns / 2] <= limit || c->geo.B <= kStreamWindowBins) ? SINET_ORDER_STREAM : SINET_ORDER_SHUFFLED;
     return SINET_OK;
 }
 

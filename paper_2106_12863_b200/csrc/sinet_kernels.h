@@ -17,7 +17,7 @@ cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st)
 
 cudaError_t setup_hist_stream();
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st);
-constexpr uint32_t kStreamWindowBins = 8192;
+constexpr uint32_t kStreamWindowBins = 4096;   // smallest ring of the stream kernel (AUTO probe threshold)
 
 cudaError_t launch_rebin(const unsigned long long* bins, uint64_t lo, uint64_t hi, uint64_t factor,
                          unsigned long long* out, uint64_t n_out, int sm_count, cudaStream_t st);

@@ -5,7 +5,7 @@
 
 namespace sinet {
 
-constexpr uint32_t kTileBins = 512;        // bins per claim tile (16 KB of u64[4] bins)
+constexpr uint32_t kTileBins = 256;        // bins per claim tile (8 KB of u64[4] bins)
 constexpr uint32_t kClsWords = 4096;       // 65536 /16 blocks x 2 bits
 constexpr uint32_t kRankWords = 2048;      // 4096 u16 prefix counts
 // staged beyond the class table + rank (24 KB): level 2 + entries + boundaries if they fit here

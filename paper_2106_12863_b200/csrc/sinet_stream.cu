@@ -22,6 +22,8 @@
 #include "sinet_device.cuh"
 #include "sinet_kernels.h"
 
+#include <cstdlib>
+
 namespace sinet {
 
 namespace {
@@ -127,25 +129,36 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
 // classified, and the tiles are retired (stored or added) right after.  A CTA
 // never waits on another CTA's tile while it holds an unreleased claim, so
 // the protocol cannot deadlock.
-template <int THREADS, int WS, bool kAgg>
+template <int THREADS, int NG, int WS, bool kAgg, bool kW1>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
+    constexpr int GT = THREADS / NG;          // threads per group
     constexpr int NW = THREADS / 32;
+    constexpr int GW = GT / 32;               // warps per group
     constexpr uint32_t NT = WS / kTileBins;
     static_assert((WS & (WS - 1)) == 0 && WS % kTileBins == 0, "window must be a power of two of tiles");
-    static_assert(NT <= (uint32_t)THREADS && (NT & (NT - 1)) == 0, "tiles per window: power of two <= threads");
+    static_assert(NT <= (uint32_t)GT && (NT & (NT - 1)) == 0, "tiles per window: power of two <= group threads");
+    static_assert(NG == 1 || NG == 2, "one or two groups per CTA");
     constexpr uint32_t kHist = NT / 2 - 1;   // tiles of history kept below a chunk's newest tile
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* s_win = smem;
-    __shared__ uint32_t s_red[2][2][NW];
-    __shared__ uint32_t s_state[NT];     // (t+1) << 2 | claim outcome
+    __shared__ uint32_t s_red_all[NG][2][2][GW];
+    __shared__ uint32_t s_state_all[NG][NT];   // (t+1) << 2 | claim outcome, per group
     __shared__ unsigned long long s_tot[NW * 12];
 
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    // NG independent groups per CTA, each with its own ring and half of the CTA's records;
+    // the lookup table is shared.  A group synchronises on its own named barrier.
+    const uint32_t gid = threadIdx.x / GT, tid = threadIdx.x % GT, lane = tid & 31u, warp = tid >> 5;
+    uint32_t* s_win = smem + gid * (WS * 6);
+    uint32_t (*s_red)[2][GW] = s_red_all[gid];
+    uint32_t* s_state = s_state_all[gid];
+    auto group_sync = [&]() {
+        if (NG == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1u + gid), "r"((uint32_t)GT) : "memory");
+    };
     const uint32_t prev_word = p.epoch > 1 ? (((p.epoch - 1u) << 2) | kTileInit) : 0u;
-    for (uint32_t i = tid; i < (uint32_t)WS * 6u / 4u; i += THREADS)
-        reinterpret_cast<uint4*>(s_win)[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid < NT) s_state[tid] = 0u;
-    const Table T = stage_table(p, s_win + WS * 6);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)NG * WS * 6u / 4u; i += THREADS)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (threadIdx.x < NG * NT) s_state_all[threadIdx.x / NT][threadIdx.x % NT] = 0u;
+    const Table T = stage_table(p, smem + NG * WS * 6);
     __syncthreads();
 
     uint32_t lo_t = 0, act_t = 0;   // resident tiles [lo_t, lo_t+NT); [lo_t, act_t) claimed, to retire
@@ -194,7 +207,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t st = s_state[slot];
             const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
             if (o == kBusy) { busy = true; continue; }
-            for (uint32_t i = tid; i < kTileBins; i += THREADS) {
+            for (uint32_t i = tid; i < kTileBins; i += GT) {
                 const uint32_t bin = t * kTileBins + i;
                 uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
                 const uint2 c = *reinterpret_cast<const uint2*>(s);
@@ -216,7 +229,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                 *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
             }
         }
-        __syncthreads();
+        group_sync();
         // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones
         if (tid < nt) {
             const uint32_t t = t_from + tid;
@@ -236,13 +249,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             }
         }
         if (busy) {
-            __syncthreads();
+            group_sync();
             for (uint32_t k = 0; k < nt; ++k) {
                 const uint32_t t = t_from + k, slot = t & (NT - 1);
                 if (!touched(t)) continue;
                 const uint32_t st = s_state[slot];
                 if (((st >> 2) == t + 1u) && (st & 3u) != kBusy) continue;
-                for (uint32_t i = tid; i < kTileBins; i += THREADS) {
+                for (uint32_t i = tid; i < kTileBins; i += GT) {
                     const uint32_t bin = t * kTileBins + i;
                     uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
                     const uint2 c = *reinterpret_cast<const uint2*>(s);
@@ -260,7 +273,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                     *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
                 }
             }
-            __syncthreads();
+            group_sync();
         }
     };
     // claim synchronously (non-blocking CASes, resolved at once) and retire [t_from, t_to)
@@ -269,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t e = (t_to - base < NT) ? t_to : base + NT;
             issue_claims(base, e);
             resolve_pending();
-            __syncthreads();
+            group_sync();
             retire(base, e);
         }
     };
@@ -285,10 +298,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (hi) atomicAdd(s + 4, hi);
     };
 
-    // this CTA's contiguous range of 4-record groups (virtual index space)
+    // this group's contiguous range of 4-record groups (virtual index space)
     const uint64_t ngroups = (p.nv + 3) / 4;
-    const uint64_t g0 = ngroups * blockIdx.x / gridDim.x;
-    const uint64_t g1 = ngroups * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t c0 = ngroups * blockIdx.x / gridDim.x, c1 = ngroups * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t g0 = c0 + (c1 - c0) * gid / NG, g1 = c0 + (c1 - c0) * (gid + 1) / NG;
 
     WarpTotals tot;
     tot.zero();
@@ -296,10 +309,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     if (g0 + tid < g1) load4(p, (g0 + tid) * 4, cur);
     uint32_t parity = 0;
 
-    for (uint64_t cbase = g0; cbase < g1; cbase += THREADS, parity ^= 1u) {
+    for (uint64_t cbase = g0; cbase < g1; cbase += GT, parity ^= 1u) {
         const uint64_t my_g = cbase + tid;
         const bool have = my_g < g1;
-        if (cbase + THREADS + tid < g1) load4(p, (cbase + THREADS + tid) * 4, nxt);   // prefetch
+        // every record of the chunk valid (all but the CTA's ragged ends): no per-record checks
+        const bool full = cbase * 4 >= p.head && (cbase + GT) * 4 <= p.nv && cbase + GT <= g1;
+        const bool tags_on = p.tags != nullptr;
+        if (cbase + GT + tid < g1) load4(p, (cbase + GT + tid) * 4, nxt);   // prefetch
 
         // ---- a3-a5: classify and map this chunk (the claims issued last chunk resolve meanwhile)
         uint32_t bin4[4], dir4[4];
@@ -307,31 +323,38 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         uint32_t tag4 = 0, bmin = 0xFFFFFFFFu, bmax = 0u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const bool valid = have && vvalid(p, my_g * 4 + j);
+            const bool valid = full || (have && vvalid(p, my_g * 4 + j));
             const uint32_t s_in = member(cur.src[j], T);
             const uint32_t d_in = member(cur.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
             const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
             uint32_t bin = 0;
-            const bool inw = map_bin(cur.ts[j], p, bin);
+            bool inw;
+            if (kW1) {   // 1 ms bins: the key is the offset itself
+                const uint64_t d = cur.ts[j] - p.start;
+                inw = d < (uint64_t)p.window;
+                bin = (uint32_t)d;
+            } else {
+                inw = map_bin(cur.ts[j], p, bin);
+            }
             const bool directed = valid && dir < 2u;
             binned4[j] = directed && inw;
             bin4[j] = bin;
             dir4[j] = dir;
             if (binned4[j]) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
-            tag4 |= (s_in | (d_in << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
+            if (tags_on) tag4 |= (s_in | (d_in << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
             tot.add(valid, cell, directed && !inw, dir, cur.by[j]);
         }
-        if (p.tags && have) store_tags4(p, my_g * 4, tag4);
+        if (tags_on && have) store_tags4(p, my_g * 4, tag4);
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
         if (lane == 0) { s_red[parity][0][warp] = bmin; s_red[parity][1][warp] = bmax; }
         resolve_pending();
-        __syncthreads();
+        group_sync();
         bmin = 0xFFFFFFFFu;
         bmax = 0u;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) { bmin = min(bmin, s_red[parity][0][w]); bmax = max(bmax, s_red[parity][1][w]); }
+        for (int w = 0; w < GW; ++w) { bmin = min(bmin, s_red[parity][0][w]); bmax = max(bmax, s_red[parity][1][w]); }
         const bool any = bmin <= bmax;
         const uint32_t bmin_t = bmin / kTileBins, bmax_t = bmax / kTileBins;
 
@@ -355,7 +378,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         }
         // warp aggregation of equal (bin, dir) keys only where the chunk is denser
         // than one record per bin (hot bins, bursts); block-uniform decision
-        const bool agg = kAgg && any && (bmax - bmin) < (uint32_t)(THREADS * 4);
+        const bool agg = kAgg && any && (bmax - bmin) < (uint32_t)(GT * 4);
         const bool key32 = p.nbins < 0x40000000u;   // keys 2*bin+dir stay below the lane sentinels
 
         // ---- a6 (accumulate): reduce the chunk into the ring
@@ -390,7 +413,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             }
             const bool in_ring = act && (bin4[j] / kTileBins - lo_t < NT);
             if (in_ring) accumulate(bin4[j], dir4[j], cnt, byt);
-            spill_warp(p, act && !in_ring, bin4[j], dir4[j], cnt, byt);
+            if (__any_sync(kFull, act && !in_ring)) spill_warp(p, act && !in_ring, bin4[j], dir4[j], cnt, byt);
         }
         cur = nxt;
 
@@ -407,40 +430,64 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 
     // retire everything still resident
     resolve_pending();
-    __syncthreads();
+    group_sync();
     if (have_window) {
         retire(lo_t, act_t);
         claim_and_retire(act_t, lo_t + NT);
     }
+    __syncthreads();
     flush_totals(tot, p.totals, s_tot);
 }
 
 // ---------------------------------------------------------------- launch
 namespace {
 constexpr int kStreamThreads = 512;
-constexpr int kStreamWS = 8192;
-
-size_t stream_smem(const KernelParams& p) {
-    return (size_t)kStreamWS * 6u * 4u + table_smem_bytes(p.nbnd, p.n_mixed, p.small);
-}
+// two layouts of the same 192 KB of ring: one group with an 8192-bin ring (sparse input:
+// a 2048-record chunk spans many ms) or two independent groups with 4096-bin rings
+// (dense input: one group's barrier/retire phase overlaps the other's loads and lookups)
+constexpr int kRingBins1 = 8192;
+constexpr int kRingBins2 = 4096;
 }  // namespace
 
+#define SINET_STREAM_KERNEL(G, A, W) k_hist_stream<kStreamThreads, G, (G == 1 ? kRingBins1 : kRingBins2), A, W>
+
 cudaError_t setup_hist_stream() {
-    const size_t mx = (size_t)kStreamWS * 6u * 4u + kMaxTableSmem;
-    cudaError_t e = cudaFuncSetAttribute(k_hist_stream<kStreamThreads, kStreamWS, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    const int mx = (int)((size_t)kRingBins1 * 6u * 4u + kMaxTableSmem);
+    cudaError_t e;
+#define SET(G, A, W)                                                                                 \
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_hist_stream<kStreamThreads, kStreamWS, false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    SET(1, true, true) SET(1, true, false) SET(1, false, true) SET(1, false, false)
+    SET(2, true, true) SET(2, true, false) SET(2, false, true) SET(2, false, false)
+#undef SET
+    return cudaSuccess;
+}
+
+int stream_groups_for(const KernelParams& p) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = std::getenv("SINET_STREAM_GROUPS");
+        forced = e ? std::atoi(e) : 0;
+    }
+    if (forced == 1 || forced == 2) return forced;
+    // records per bin of the window: >= 3/4 -> two groups (a 1024-record chunk spans few tiles)
+    return (p.n * 4 >= (uint64_t)p.nbins * 3) ? 2 : 1;
 }
 
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st) {
-    const size_t sm = stream_smem(p);
-    // one CTA per SM, but never more CTAs than chunks' worth of records
-    uint64_t chunks = (p.nv / 4 + kStreamThreads - 1) / kStreamThreads;
-    int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
-    if (agg) k_hist_stream<kStreamThreads, kStreamWS, true><<<grid, kStreamThreads, sm, st>>>(p);
-    else k_hist_stream<kStreamThreads, kStreamWS, false><<<grid, kStreamThreads, sm, st>>>(p);
+    static_assert(kRingBins1 == 2 * kRingBins2, "both layouts use the same shared memory");
+    const size_t sm = (size_t)kRingBins1 * 6u * 4u + table_smem_bytes(p.nbnd, p.n_mixed, p.small);
+    const uint64_t chunks = (p.nv / 4 + kStreamThreads - 1) / kStreamThreads;
+    const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
+    const bool w1 = p.width == 1u;
+    const int g = stream_groups_for(p);
+#define LAUNCH(G)                                                                               \
+    if (agg && w1) SINET_STREAM_KERNEL(G, true, true)<<<grid, kStreamThreads, sm, st>>>(p);      \
+    else if (agg) SINET_STREAM_KERNEL(G, true, false)<<<grid, kStreamThreads, sm, st>>>(p);      \
+    else if (w1) SINET_STREAM_KERNEL(G, false, true)<<<grid, kStreamThreads, sm, st>>>(p);       \
+    else SINET_STREAM_KERNEL(G, false, false)<<<grid, kStreamThreads, sm, st>>>(p);
+    if (g == 2) { LAUNCH(2) } else { LAUNCH(1) }
+#undef LAUNCH
     return cudaGetLastError();
 }
 
