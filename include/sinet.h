@@ -241,6 +241,10 @@ int sinet_last_strategy(const sinet_ctx* ctx);
  * Errors: E_INVAL as sinet_open's table checks. */
 int sinet_table_member_host(const uint32_t* prefix_net, const uint8_t* prefix_len, uint32_t n_prefixes,
                             const uint32_t* ips, uint64_t n, uint8_t* out);
+/* Performance knobs of the STREAM kernel (results are identical for every setting):
+ * stream_groups 0 = automatic, 1 = one 8192-bin ring per CTA, 2 = two independent
+ * 4096-bin rings per CTA; warp_aggregation 1/0 = on/off, -1 = unchanged.  Errors: E_INVAL. */
+int sinet_set_tuning(sinet_ctx* ctx, int stream_groups, int warp_aggregation);
 /* Compile-time constants of this build. */
 uint32_t sinet_tile_bins(void);
 int sinet_abi_version(void);

@@ -131,6 +131,7 @@ struct sinet_ctx {
     int last_strategy = 0;
     int auto_choice = 0;          // strategy AUTO resolved by the first probe
     bool agg = true;              // warp aggregation of equal keys in the stream kernel
+    uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint64_t launches = 0;
     ncclComm_t comm = nullptr;
     // host-streaming pipeline
@@ -190,6 +191,7 @@ KernelParams base_params(sinet_ctx* c) {
     p.n_mixed = c->table.n_mixed;
     p.nbnd = c->nbnd;
     p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
+    p.stream_groups = c->stream_groups;
     p.lut = c->lut;
     p.start = c->cfg.window_start_ms;
     p.window = (uint32_t)c->cfg.window_ms;
@@ -365,6 +367,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     OPEN_CUDA(setup_hist_atomic());
     OPEN_CUDA(setup_hist_stream());
     if (const char* a = std::getenv("SINET_AGG")) c->agg = std::atoi(a) != 0;
+    if (const char* g = std::getenv("SINET_STREAM_GROUPS")) c->stream_groups = (uint32_t)std::atoi(g);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
@@ -678,6 +681,15 @@ int sinet_table_member_host(const uint32_t* net, const uint8_t* len, uint32_t np
 const char* sinet_last_error(const sinet_ctx* c) { return c ? c->err.c_str() : "NULL ctx"; }
 uint64_t sinet_launch_count(const sinet_ctx* c) { return c ? c->launches : 0; }
 int sinet_last_strategy(const sinet_ctx* c) { return c ? c->last_strategy : 0; }
+
+int sinet_set_tuning(sinet_ctx* c, int stream_groups, int warp_aggregation) {
+    if (!c) return SINET_E_INVAL;
+    if (stream_groups < 0 || stream_groups > 2 || warp_aggregation < -1 || warp_aggregation > 1)
+        return fail(c, SINET_E_INVAL, "stream_groups must be 0, 1 or 2; warp_aggregation -1, 0 or 1");
+    c->stream_groups = (uint32_t)stream_groups;
+    if (warp_aggregation >= 0) c->agg = warp_aggregation != 0;
+    return SINET_OK;
+}
 
 int sinet_set_kernel_timing(sinet_ctx* c, int on) {
     if (!c) return SINET_E_INVAL;

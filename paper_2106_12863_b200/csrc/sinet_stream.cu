@@ -22,8 +22,6 @@
 #include "sinet_device.cuh"
 #include "sinet_kernels.h"
 
-#include <cstdlib>
-
 namespace sinet {
 
 namespace {
@@ -464,12 +462,7 @@ cudaError_t setup_hist_stream() {
 }
 
 int stream_groups_for(const KernelParams& p) {
-    static int forced = -1;
-    if (forced < 0) {
-        const char* e = std::getenv("SINET_STREAM_GROUPS");
-        forced = e ? std::atoi(e) : 0;
-    }
-    if (forced == 1 || forced == 2) return forced;
+    if (p.stream_groups == 1 || p.stream_groups == 2) return (int)p.stream_groups;
     // records per bin of the window: >= 3/4 -> two groups (a 1024-record chunk spans few tiles)
     return (p.n * 4 >= (uint64_t)p.nbins * 3) ? 2 : 1;
 }

@@ -237,6 +237,10 @@ class SinetHistogram:
     def last_strategy(self) -> int:
         return int(lib.sinet_last_strategy(self.ctx))
 
+    def set_tuning(self, stream_groups: int = 0, warp_aggregation: int = -1):
+        """Stream-kernel layout (0 auto / 1 / 2 groups) and warp aggregation (1/0, -1 unchanged)."""
+        check(lib.sinet_set_tuning(self.ctx, stream_groups, warp_aggregation), self.ctx, "set_tuning")
+
     def set_kernel_timing(self, on: bool):
         check(lib.sinet_set_kernel_timing(self.ctx, 1 if on else 0), self.ctx, "timing")
 

@@ -34,8 +34,9 @@ def dev_cols(cols, device="cuda"):
 
 
 def gpu_run(S, nets, lens, cols, start, window, width=1, lut=LUT_SRC_PRIORITY, order=0, chunks=None,
-            tags=False):
+            tags=False, groups=0, agg=-1):
     h = S.SinetHistogram(nets, lens, start, window, width, lut=lut, order=order)
+    h.set_tuning(groups, agg)
     d = dev_cols(cols)
     n = d[0].numel()
     tg = torch.full((max(n, 4),), 0xEE, dtype=torch.uint8, device="cuda") if tags else None
@@ -84,15 +85,15 @@ def _adversarial(n, nets, lens, start, window, seed):
     return ts, pick(), pick(), nb
 
 
-@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("order,groups", [(1, 1), (1, 2), (2, 0)])
 @pytest.mark.parametrize("lut", [LUT_SRC_PRIORITY, LUT_ALG1, LUT_STRICT])
 @pytest.mark.parametrize("width", [1, 3, 1000])
-def test_adversarial_parity(S, oracle_lib, lut, width, order):
+def test_adversarial_parity(S, oracle_lib, lut, width, order, groups):
     nets, lens = prefix_table(WORKLOADS["c1"])
     start, window = 1_613_660_400_000, 3_000_000
     for n in (1, 5, 127, 129, 40_001):   # ragged tails around the 4-record / 128-record groups
         cols = _adversarial(n, nets, lens, start, window, seed=n + width)
-        g = gpu_run(S, nets, lens, cols, start, window, width, lut, order=order, tags=True)
+        g = gpu_run(S, nets, lens, cols, start, window, width, lut, order=order, tags=True, groups=groups)
         o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, width, lut=lut)
         assert_parity(g, o)
         np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
@@ -105,30 +106,43 @@ def test_c1_full_parity(S, oracle_lib, wl_name, order):
     wl = WORKLOADS[wl_name].with_(order=order)
     nets, lens = prefix_table(wl)
     cols = to_numpy(records(wl))
-    for strategy in (0, 1, 2):
-        g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy)
-        o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    for strategy, groups, agg in ((0, 0, -1), (1, 1, 1), (1, 2, 1), (1, 2, 0), (2, 0, -1)):
+        g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy, groups=groups, agg=agg)
         assert_parity(g, o)
 
 
-@pytest.mark.parametrize("strategy", [1, 2])
-def test_bursty_hot_bins(S, oracle_lib, strategy):
+@pytest.mark.parametrize("groups", [1, 2])
+def test_dense_stream_both_layouts(S, oracle_lib, groups):
+    """A dense stream (C2 density: ~1.2 records per ms) through both ring layouts."""
+    wl = WORKLOADS["c2"].with_(n=4_000_000, window_ms=3_600_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=1, groups=groups, tags=True)
+    assert_parity(g, o)
+    np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
+                                                             wl.window_start_ms, wl.window_ms))
+
+
+@pytest.mark.parametrize("strategy,groups", [(1, 1), (1, 2), (2, 0)])
+def test_bursty_hot_bins(S, oracle_lib, strategy, groups):
     """C4-shaped (diurnal + Zipf bursts + 1 % in one ms) and a degenerate all-in-one-ms batch."""
     wl = WORKLOADS["c4"].with_(n=2_000_000)
     nets, lens = prefix_table(wl)
     cols = to_numpy(records(wl))
-    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy)
+    g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy, groups=groups)
     o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
     assert_parity(g, o)
     ts, src, dst, nb = cols
     one = (np.full_like(ts, wl.window_start_ms + 43_200_000), src, dst, nb)
-    g = gpu_run(S, nets, lens, one, wl.window_start_ms, wl.window_ms, order=strategy)
+    g = gpu_run(S, nets, lens, one, wl.window_start_ms, wl.window_ms, order=strategy, groups=groups)
     o = oracle_lib.classify_histogram(*one, nets, lens, wl.window_start_ms, wl.window_ms, 1)
     assert_parity(g, o)
 
 
-@pytest.mark.parametrize("strategy", [1, 2])
-def test_gaps_and_window_jumps(S, oracle_lib, strategy):
+@pytest.mark.parametrize("strategy,groups", [(1, 1), (1, 2), (2, 0)])
+def test_gaps_and_window_jumps(S, oracle_lib, strategy, groups):
     """Sparse records hours apart (window jumps), then a dense stretch, in one batch."""
     rng = np.random.default_rng(77)
     nets, lens = prefix_table(WORKLOADS["c2"])
@@ -142,7 +156,7 @@ def test_gaps_and_window_jumps(S, oracle_lib, strategy):
     dst = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
     nb = rng.integers(0, 1 << 34, n, dtype=np.uint64)
     cols = (ts, src, dst, nb)
-    g = gpu_run(S, nets, lens, cols, start, window, order=strategy)
+    g = gpu_run(S, nets, lens, cols, start, window, order=strategy, groups=groups)
     o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, 1)
     assert_parity(g, o)
 
