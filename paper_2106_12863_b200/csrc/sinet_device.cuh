@@ -70,21 +70,26 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
     return (uint64_t)a + ((uint64_t)b << 24) + ((uint64_t)c << 48);
 }
 
-// Per-thread accumulators (predicated adds: ~16 thread-instructions per record,
-// half a warp-instruction per record), reduced once per CTA at the end.
+// Per-thread accumulators of the side totals.  Instead of one counter pair per
+// membership cell, keep sums over {all, s_in, d_in, s_in&d_in} (fewer predicated
+// adds); the 2x2 matrix follows by inclusion-exclusion (mod 2^64) at the end.
 struct WarpTotals {
-    uint32_t mc[4], oc[2];
-    uint64_t mb[4], ob[2];
+    uint32_t cT, cS, cD, cSD, oc[2];
+    uint64_t bT, bS, bD, bSD, ob[2];
     __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { mc[k] = 0; mb[k] = 0; }
-        oc[0] = oc[1] = 0;
-        ob[0] = ob[1] = 0;
+        cT = cS = cD = cSD = 0u;
+        bT = bS = bD = bSD = 0ull;
+        oc[0] = oc[1] = 0u;
+        ob[0] = ob[1] = 0ull;
     }
     __device__ __forceinline__ void add(bool valid, uint32_t cell, bool oow, uint32_t dir, uint64_t b) {
-#pragma unroll
-        for (uint32_t k = 0; k < 4; ++k)
-            if (valid && cell == k) { mc[k] += 1u; mb[k] += b; }
+        if (valid) {
+            const bool s = cell & 2u, d = cell & 1u;
+            cT += 1u; bT += b;
+            if (s) { cS += 1u; bS += b; }
+            if (d) { cD += 1u; bD += b; }
+            if (s && d) { cSD += 1u; bSD += b; }
+        }
         if (oow) {
             if (dir == 0u) { oc[0] += 1u; ob[0] += b; } else { oc[1] += 1u; ob[1] += b; }
         }
@@ -96,15 +101,15 @@ __device__ __forceinline__ void flush_totals(const WarpTotals& t, unsigned long 
                                              unsigned long long* s_scratch /* [32][12] */) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     unsigned long long v[12];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        v[k] = __reduce_add_sync(kFull, t.mc[k]);
-        v[4 + k] = warp_sum_u64(t.mb[k]);
+    {
+        const unsigned long long cT = __reduce_add_sync(kFull, t.cT), cS = __reduce_add_sync(kFull, t.cS);
+        const unsigned long long cD = __reduce_add_sync(kFull, t.cD), cSD = __reduce_add_sync(kFull, t.cSD);
+        const unsigned long long bT = warp_sum_u64(t.bT), bS = warp_sum_u64(t.bS);
+        const unsigned long long bD = warp_sum_u64(t.bD), bSD = warp_sum_u64(t.bSD);
+        // cells s_in*2+d_in: 0 = neither, 1 = d only, 2 = s only, 3 = both (mod 2^64)
+        v[0] = cT - cS - cD + cSD; v[1] = cD - cSD; v[2] = cS - cSD; v[3] = cSD;
+        v[4] = bT - bS - bD + bSD; v[5] = bD - bSD; v[6] = bS - bSD; v[7] = bSD;
     }
-    v[8] = __reduce_add_sync(kFull, t.oc[0]);
-    v[9] = __reduce_add_sync(kFull, t.oc[1]);
-    v[10] = warp_sum_u64(t.ob[0]);
-    v[11] = warp_sum_u64(t.ob[1]);
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < 12; ++k) s_scratch[warp * 12 + k] = v[k];
@@ -170,6 +175,9 @@ __device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t vbas
 // Stage the /16 class table and the mixed-block rank (and, for small lists, the
 // level-2 classes, entries and boundaries) into shared memory at `smem`
 // (table_smem_bytes() bytes).
+// kSmall (compile-time, = p.small) lets the compiler see the level-2 / entry / boundary
+// pointers as shared memory (LDS) rather than generic loads.
+template <bool kSmall>
 __device__ __forceinline__ Table stage_table(const KernelParams& p, uint32_t* smem) {
     Table T;
     const uint4* g4 = reinterpret_cast<const uint4*>(p.cls2);
@@ -179,7 +187,7 @@ __device__ __forceinline__ Table stage_table(const KernelParams& p, uint32_t* sm
     for (uint32_t i = threadIdx.x; i < kRankWords; i += blockDim.x) s_rank[i] = __ldg(p.rank + i);
     T.cls2 = smem;
     T.rank = reinterpret_cast<const uint16_t*>(s_rank);
-    if (p.small) {
+    if (kSmall) {
         uint32_t* s_l2 = s_rank + kRankWords;
         uint32_t* s_me = s_l2 + 16u * p.n_mixed;
         uint32_t* s_bnd = s_me + p.n_mixed;

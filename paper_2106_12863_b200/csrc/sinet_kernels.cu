@@ -39,10 +39,11 @@ __global__ void __launch_bounds__(256) k_materialize(ulonglong2* bins, uint32_t*
 // Persistent grid; each warp takes 128 consecutive records per step (4 per
 // lane, vector loads), so the loop is warp-uniform and the totals can use
 // warp ballots/reductions.
+template <bool kSmall>
 __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_tot[32 * 12];
-    const Table T = stage_table(p, smem);
+    const Table T = stage_table<kSmall>(p, smem);
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -92,19 +93,24 @@ cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32
 }
 
 cudaError_t setup_hist_atomic() {
-    return cudaFuncSetAttribute(k_hist_atomic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kMaxTableSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_hist_atomic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kMaxTableSmem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_hist_atomic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxTableSmem);
 }
 
 int hist_atomic_blocks_per_sm(const KernelParams& p) {
     int nb = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic, 256,
-                                                                  table_smem_bytes(p.nbnd, p.n_mixed, p.small));
+    const size_t sm = table_smem_bytes(p.nbnd, p.n_mixed, p.small);
+    cudaError_t e = p.small ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic<true>, 256, sm)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hist_atomic<false>, 256, sm);
     return (e == cudaSuccess && nb > 0) ? nb : 1;
 }
 
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st) {
-    k_hist_atomic<<<grid, 256, table_smem_bytes(p.nbnd, p.n_mixed, p.small), st>>>(p);
+    const size_t sm = table_smem_bytes(p.nbnd, p.n_mixed, p.small);
+    if (p.small) k_hist_atomic<true><<<grid, 256, sm, st>>>(p);
+    else k_hist_atomic<false><<<grid, 256, sm, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -20,11 +20,12 @@
 
 namespace sinet {
 
+template <bool kSmall>
 __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t sentinel, uint32_t* keys,
                                                   unsigned long long* vals) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_tot[32 * 12];
-    const Table T = stage_table(p, smem);
+    const Table T = stage_table<kSmall>(p, smem);
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t wpb = blockDim.x >> 5;
@@ -139,9 +140,11 @@ cudaError_t launch_sortreduce(const KernelParams& p, void* scratch, size_t scrat
     int* nruns = reinterpret_cast<int*>(s + L.nruns);
     void* temp = s + L.temp;
     const size_t smem = table_smem_bytes(p.nbnd, p.n_mixed, p.small);
-    cudaError_t e = cudaFuncSetAttribute(k_map_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = p.small ? cudaFuncSetAttribute(k_map_keys<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                            : cudaFuncSetAttribute(k_map_keys<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_map_keys<<<sm_count * 4, 256, smem, st>>>(p, sentinel, keys_in, vals_in);
+    if (p.small) k_map_keys<true><<<sm_count * 4, 256, smem, st>>>(p, sentinel, keys_in, vals_in);
+    else k_map_keys<false><<<sm_count * 4, 256, smem, st>>>(p, sentinel, keys_in, vals_in);
     size_t t = tb;
     const int ni = (int)n;
     if ((e = cub::DeviceRadixSort::SortPairs(temp, t, keys_in, keys_out, vals_in, vals_out, ni, 0, eb, st))) return e;

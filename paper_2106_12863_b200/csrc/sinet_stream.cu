@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
 // classified, and the tiles are retired (stored or added) right after.  A CTA
 // never waits on another CTA's tile while it holds an unreleased claim, so
 // the protocol cannot deadlock.
-template <int THREADS, int NG, int WS, bool kAgg, bool kW1>
+template <int THREADS, int NG, int WS, bool kAgg, bool kW1, bool kSmall>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     constexpr int GT = THREADS / NG;          // threads per group
     constexpr int NW = THREADS / 32;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     for (uint32_t i = threadIdx.x; i < (uint32_t)NG * WS * 6u / 4u; i += THREADS)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (threadIdx.x < NG * NT) s_state_all[threadIdx.x / NT][threadIdx.x % NT] = 0u;
-    const Table T = stage_table(p, smem + NG * WS * 6);
+    const Table T = stage_table<kSmall>(p, smem + NG * WS * 6);
     __syncthreads();
 
     uint32_t lo_t = 0, act_t = 0;   // resident tiles [lo_t, lo_t+NT); [lo_t, act_t) claimed, to retire
@@ -301,6 +301,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     const uint64_t c0 = ngroups * blockIdx.x / gridDim.x, c1 = ngroups * (blockIdx.x + 1) / gridDim.x;
     const uint64_t g0 = c0 + (c1 - c0) * gid / NG, g1 = c0 + (c1 - c0) * (gid + 1) / NG;
 
+    // chunks whose every record is valid: not the batch's ragged first/last 4-record group
+    const uint64_t full_lo = (p.head != 0u) ? 1u : 0u;
+    const uint64_t full_hi = (g1 * 4 > p.nv) ? g1 - 1 : g1;
     WarpTotals tot;
     tot.zero();
     Rec4 cur, nxt;
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         const uint64_t my_g = cbase + tid;
         const bool have = my_g < g1;
         // every record of the chunk valid (all but the CTA's ragged ends): no per-record checks
-        const bool full = cbase * 4 >= p.head && (cbase + GT) * 4 <= p.nv && cbase + GT <= g1;
+        const bool full = cbase >= full_lo && cbase + GT <= full_hi;
         const bool tags_on = p.tags != nullptr;
         if (cbase + GT + tid < g1) load4(p, (cbase + GT + tid) * 4, nxt);   // prefetch
 
@@ -447,16 +450,17 @@ constexpr int kRingBins1 = 8192;
 constexpr int kRingBins2 = 4096;
 }  // namespace
 
-#define SINET_STREAM_KERNEL(G, A, W) k_hist_stream<kStreamThreads, G, (G == 1 ? kRingBins1 : kRingBins2), A, W>
+#define SINET_STREAM_KERNEL(G, A, W, S) k_hist_stream<kStreamThreads, G, (G == 1 ? kRingBins1 : kRingBins2), A, W, S>
 
 cudaError_t setup_hist_stream() {
     const int mx = (int)((size_t)kRingBins1 * 6u * 4u + kMaxTableSmem);
     cudaError_t e;
-#define SET(G, A, W)                                                                                 \
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
+#define SET(G, A, W, S)                                                                                 \
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W, S), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
-    SET(1, true, true) SET(1, true, false) SET(1, false, true) SET(1, false, false)
-    SET(2, true, true) SET(2, true, false) SET(2, false, true) SET(2, false, false)
+#define SET4(G, S) SET(G, true, true, S) SET(G, true, false, S) SET(G, false, true, S) SET(G, false, false, S)
+    SET4(1, true) SET4(1, false) SET4(2, true) SET4(2, false)
+#undef SET4
 #undef SET
     return cudaSuccess;
 }
@@ -474,12 +478,13 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
     const bool w1 = p.width == 1u;
     const int g = stream_groups_for(p);
-#define LAUNCH(G)                                                                               \
-    if (agg && w1) SINET_STREAM_KERNEL(G, true, true)<<<grid, kStreamThreads, sm, st>>>(p);      \
-    else if (agg) SINET_STREAM_KERNEL(G, true, false)<<<grid, kStreamThreads, sm, st>>>(p);      \
-    else if (w1) SINET_STREAM_KERNEL(G, false, true)<<<grid, kStreamThreads, sm, st>>>(p);       \
-    else SINET_STREAM_KERNEL(G, false, false)<<<grid, kStreamThreads, sm, st>>>(p);
-    if (g == 2) { LAUNCH(2) } else { LAUNCH(1) }
+#define LAUNCH(G, S)                                                                                \
+    if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S)<<<grid, kStreamThreads, sm, st>>>(p);       \
+    else if (agg) SINET_STREAM_KERNEL(G, true, false, S)<<<grid, kStreamThreads, sm, st>>>(p);       \
+    else if (w1) SINET_STREAM_KERNEL(G, false, true, S)<<<grid, kStreamThreads, sm, st>>>(p);        \
+    else SINET_STREAM_KERNEL(G, false, false, S)<<<grid, kStreamThreads, sm, st>>>(p);
+    if (g == 2) { if (p.small) { LAUNCH(2, true) } else { LAUNCH(2, false) } }
+    else { if (p.small) { LAUNCH(1, true) } else { LAUNCH(1, false) } }
 #undef LAUNCH
     return cudaGetLastError();
 }
