@@ -110,6 +110,10 @@ __device__ __forceinline__ void flush_totals(const WarpTotals& t, unsigned long 
         v[0] = cT - cS - cD + cSD; v[1] = cD - cSD; v[2] = cS - cSD; v[3] = cSD;
         v[4] = bT - bS - bD + bSD; v[5] = bD - bSD; v[6] = bS - bSD; v[7] = bSD;
     }
+    v[8] = __reduce_add_sync(kFull, t.oc[0]);
+    v[9] = __reduce_add_sync(kFull, t.oc[1]);
+    v[10] = warp_sum_u64(t.ob[0]);
+    v[11] = warp_sum_u64(t.ob[1]);
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < 12; ++k) s_scratch[warp * 12 + k] = v[k];

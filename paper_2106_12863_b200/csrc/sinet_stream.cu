@@ -377,9 +377,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             hull_lo = min(hull_lo, bmin_t > lo_t ? bmin_t : lo_t);
             hull_hi = max(hull_hi, bmax_t);
         }
-        // warp aggregation of equal (bin, dir) keys only where the chunk is denser
-        // than one record per bin (hot bins, bursts); block-uniform decision
-        const bool agg = kAgg && any && (bmax - bmin) < (uint32_t)(GT * 4);
         const bool key32 = p.nbins < 0x40000000u;   // keys 2*bin+dir stay below the lane sentinels
 
         // ---- a6 (accumulate): reduce the chunk into the ring
@@ -389,7 +386,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             bool act = b;
             uint32_t cnt = 1u;
             uint64_t byt = cur.by[j];
-            if (agg) {
+            // warp aggregation of equal (bin, dir) keys (hot bins, bursts): only when a
+            // cheap neighbour test finds a duplicate in the warp (records of one slot are
+            // 4 apart in stream order, so hot keys show up in adjacent lanes)
+            bool try_agg = false;
+            if (kAgg) {
+                const uint32_t k32 = b ? ((bin4[j] << 1) | dir4[j]) : 0xFFFFFFFFu - lane;
+                const uint32_t kp = __shfl_up_sync(kFull, k32, 1);
+                try_agg = __any_sync(kFull, b && lane > 0u && kp == k32);
+            }
+            if (try_agg) {
                 unsigned m;
                 if (key32) {
                     const uint32_t key = b ? ((bin4[j] << 1) | dir4[j]) : 0xFFFFFFFFu - lane;
