@@ -90,7 +90,7 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, rank, mentry, l2, flags, sparse, total;
+    size_t totals, cls2, entry, bnd, rank, mentry, l2, flags, sparse, counters, total;
 };
 
 WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
@@ -105,6 +105,7 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     L.l2 = off;     off = align_up(off + (size_t)(2u * n_prefixes + 1u) * 64, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
+    L.counters = off; off = align_up(off + 64, 256);
     L.total = off;
     return L;
 }
@@ -130,8 +131,9 @@ struct sinet_ctx {
     bool materialized = false;
     int last_strategy = 0;
     int auto_choice = 0;          // strategy AUTO resolved by the first probe
-    bool agg = true;              // warp aggregation of equal keys in the stream kernel
+    bool agg = false;             // warp aggregation of equal keys in the stream kernel (measured slower on C4)
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
+    uint32_t ranges_per_group = 0;
     uint64_t launches = 0;
     ncclComm_t comm = nullptr;
     // host-streaming pipeline
@@ -192,6 +194,8 @@ KernelParams base_params(sinet_ctx* c) {
     p.nbnd = c->nbnd;
     p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
     p.stream_groups = c->stream_groups;
+    p.ranges_per_group = c->ranges_per_group;
+    p.range_counter = ws_u32(c, c->ws.counters);
     p.lut = c->lut;
     p.start = c->cfg.window_start_ms;
     p.window = (uint32_t)c->cfg.window_ms;
@@ -368,6 +372,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     OPEN_CUDA(setup_hist_stream());
     if (const char* a = std::getenv("SINET_AGG")) c->agg = std::atoi(a) != 0;
     if (const char* g = std::getenv("SINET_STREAM_GROUPS")) c->stream_groups = (uint32_t)std::atoi(g);
+    if (const char* r = std::getenv("SINET_RANGES")) c->ranges_per_group = (uint32_t)std::atoi(r);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
@@ -382,6 +387,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     if (!c->table.l2.empty())
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.l2, c->table.l2.data(), c->table.l2.size() * 4, cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
+    OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.counters, 0, 64, c->stream));
     OPEN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         OPEN_CUDA(cudaEventCreateWithFlags(&c->copy_done[k], cudaEventDisableTiming));

@@ -39,6 +39,9 @@ struct KernelParams {
     uint32_t n_mixed;
     uint32_t small;                // 1: level 2, entries and boundaries fit in shared memory
     uint32_t stream_groups;        // 0 auto, 1 or 2: layout of the stream kernel's ring
+    uint32_t ranges_per_group;     // 0 = default: record ranges handed out per group (load balance)
+    uint32_t n_ranges;             // set by the launcher
+    uint32_t* range_counter;       // zeroed by the launcher before each launch
     uint32_t lut;                  // 4 x 2 bits, index s_in*2+d_in
     uint64_t start;                // window start (ms)
     uint32_t window;               // W (ms) < 2^32

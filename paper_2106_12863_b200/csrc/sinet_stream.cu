@@ -296,16 +296,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (hi) atomicAdd(s + 4, hi);
     };
 
-    // this group's contiguous range of 4-record groups (virtual index space)
+    // Contiguous ranges of 4-record groups (virtual index space) are handed out
+    // dynamically (one atomic per range, counter zeroed before each launch) so that
+    // groups that finish early take more.
     const uint64_t ngroups = (p.nv + 3) / 4;
-    const uint64_t c0 = ngroups * blockIdx.x / gridDim.x, c1 = ngroups * (blockIdx.x + 1) / gridDim.x;
-    const uint64_t g0 = c0 + (c1 - c0) * gid / NG, g1 = c0 + (c1 - c0) * (gid + 1) / NG;
+    const uint64_t nranges = (uint64_t)p.n_ranges;
+    __shared__ uint64_t s_range[NG];
+    WarpTotals tot;
+    tot.zero();
+    for (;;) {
+    if (tid == 0) s_range[gid] = atomicAdd(p.range_counter, 1u);
+    group_sync();
+    const uint64_t range = s_range[gid];
+    if (range >= nranges) break;
+    const uint64_t g0 = ngroups * range / nranges, g1 = ngroups * (range + 1) / nranges;
+    lo_t = 0; act_t = 0; have_window = false; hull_lo = 0xFFFFFFFFu; hull_hi = 0u;
 
     // chunks whose every record is valid: not the batch's ragged first/last 4-record group
     const uint64_t full_lo = (p.head != 0u) ? 1u : 0u;
     const uint64_t full_hi = (g1 * 4 > p.nv) ? g1 - 1 : g1;
-    WarpTotals tot;
-    tot.zero();
     Rec4 cur, nxt;
     if (g0 + tid < g1) load4(p, (g0 + tid) * 4, cur);
     uint32_t parity = 0;
@@ -442,6 +451,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         retire(lo_t, act_t);
         claim_and_retire(act_t, lo_t + NT);
     }
+    }   // ranges
     __syncthreads();
     flush_totals(tot, p.totals, s_tot);
 }
@@ -484,11 +494,17 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
     const bool w1 = p.width == 1u;
     const int g = stream_groups_for(p);
+    KernelParams q = p;   // ranges: a few per group, each at least a few chunks long
+    const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 3u);
+    const uint64_t max_r = p.nv / (4u * kStreamThreads * 4u) + 1u;
+    q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
 #define LAUNCH(G, S)                                                                                \
-    if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S)<<<grid, kStreamThreads, sm, st>>>(p);       \
-    else if (agg) SINET_STREAM_KERNEL(G, true, false, S)<<<grid, kStreamThreads, sm, st>>>(p);       \
-    else if (w1) SINET_STREAM_KERNEL(G, false, true, S)<<<grid, kStreamThreads, sm, st>>>(p);        \
-    else SINET_STREAM_KERNEL(G, false, false, S)<<<grid, kStreamThreads, sm, st>>>(p);
+    if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S)<<<grid, kStreamThreads, sm, st>>>(q);       \
+    else if (agg) SINET_STREAM_KERNEL(G, true, false, S)<<<grid, kStreamThreads, sm, st>>>(q);       \
+    else if (w1) SINET_STREAM_KERNEL(G, false, true, S)<<<grid, kStreamThreads, sm, st>>>(q);        \
+    else SINET_STREAM_KERNEL(G, false, false, S)<<<grid, kStreamThreads, sm, st>>>(q);
+    cudaError_t e = cudaMemsetAsync(p.range_counter, 0, 8, st);
+    if (e != cudaSuccess) return e;
     if (g == 2) { if (p.small) { LAUNCH(2, true) } else { LAUNCH(2, false) } }
     else { if (p.small) { LAUNCH(1, true) } else { LAUNCH(1, false) } }
 #undef LAUNCH
