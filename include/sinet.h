@@ -169,6 +169,17 @@ size_t sinet_sortreduce_scratch_bytes(const sinet_config* cfg, uint64_t n);
 int sinet_classify_histogram_sortreduce(sinet_ctx* ctx, const sinet_records* recs,
                                         void* d_scratch, size_t scratch_bytes);
 
+/* NEXT-2, watchlist filter (Figs 8-11: 300 AbuseIPDB addresses P:L345-350, 877
+ * GRIZZLY STEPPE addresses P:L366-370): from now on only records whose source OR
+ * destination equals a listed address are counted (totals and bins; tags still
+ * describe every record) -- filter, then the unchanged histogram.  The list (set
+ * semantics: duplicates collapse) is copied into the caller's device buffer of
+ * sinet_watchlist_bytes(n) bytes (16-byte aligned), which must stay valid while
+ * the filter is active.  n == 0 removes the filter.  Synchronises the stream.
+ * Errors: E_INVAL, E_CUDA. */
+size_t sinet_watchlist_bytes(uint32_t n);
+int sinet_set_watchlist(sinet_ctx* ctx, const uint32_t* ips, uint32_t n, void* d_buf, size_t buf_bytes);
+
 /* Materialise every bin (zero-fill tiles no record touched).  Idempotent;
  * called implicitly by sinet_reduce and sinet_read_bins. */
 int sinet_finalize(sinet_ctx* ctx);

@@ -58,6 +58,8 @@ def _load():
         lib.oracle_tags.argtypes = [u64p, u32p, u32p, ctypes.c_uint64, u32p, u8p, ctypes.c_uint32,
                                     ctypes.c_uint64, ctypes.c_uint64, u8p]
         lib.oracle_tags.restype = None
+        lib.oracle_watch_filter.argtypes = [u32p, u32p, ctypes.c_uint64, u32p, ctypes.c_uint32, u64p]
+        lib.oracle_watch_filter.restype = ctypes.c_uint64
         lib.oracle_rebin.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, u64p]
         lib.oracle_rebin.restype = None
         lib.oracle_sparse.argtypes = [u64p, u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
@@ -180,3 +182,22 @@ def sparse(count, nbytes, start: int, width: int):
                               _ptr(t, ctypes.c_uint64), _ptr(c, ctypes.c_uint64), _ptr(b, ctypes.c_uint64), cap)
     assert k == cap
     return t, c, b
+
+
+def watch_filter(src, dst, watchlist) -> np.ndarray:
+    """NEXT-2: indices of the records whose source or destination is listed (order kept)."""
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    wl = np.ascontiguousarray(np.asarray(watchlist, dtype=np.uint32))
+    keep = np.zeros(len(src), dtype=np.uint64)
+    k = _load().oracle_watch_filter(_ptr(src, ctypes.c_uint32), _ptr(dst, ctypes.c_uint32), len(src),
+                                    _ptr(wl, ctypes.c_uint32), len(wl), _ptr(keep, ctypes.c_uint64))
+    return keep[:k].astype(np.int64)
+
+
+def classify_histogram_watched(ts, src, dst, nbytes, nets, lens, watchlist, start, window, width,
+                               lut=LUT_SRC_PRIORITY, threads: int = 1) -> OracleResult:
+    """Filter by the watchlist (either endpoint), then the unchanged histogram."""
+    keep = watch_filter(src, dst, watchlist)
+    cols = [np.ascontiguousarray(np.asarray(c)[keep]) for c in (ts, src, dst, nbytes)]
+    return classify_histogram(*cols, nets, lens, start, window, width, lut=lut, threads=threads)

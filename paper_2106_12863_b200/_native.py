@@ -77,6 +77,8 @@ _SIGS = {
     "sinet_kernel_time": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)], _i),
     "sinet_last_strategy": ([_vp], _i),
     "sinet_set_tuning": ([_vp, _i, _i], _i),
+    "sinet_watchlist_bytes": ([_u32], ctypes.c_size_t),
+    "sinet_set_watchlist": ([_vp, _vp, _u32, _vp, ctypes.c_size_t], _i),
     "sinet_table_member_host": ([_vp, _vp, _u32, _vp, _u64, _vp], _i),
 }
 for _name, (_args, _res) in _SIGS.items():

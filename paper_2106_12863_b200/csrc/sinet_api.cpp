@@ -134,6 +134,10 @@ struct sinet_ctx {
     bool agg = false;             // warp aggregation of equal keys in the stream kernel (measured slower on C4)
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t ranges_per_group = 0;
+    // NEXT-2 watchlist (caller-owned device buffer)
+    const uint32_t* wbits = nullptr;
+    const uint32_t* wlist = nullptr;
+    uint32_t wn = 0;
     uint64_t launches = 0;
     ncclComm_t comm = nullptr;
     // host-streaming pipeline
@@ -196,6 +200,9 @@ KernelParams base_params(sinet_ctx* c) {
     p.stream_groups = c->stream_groups;
     p.ranges_per_group = c->ranges_per_group;
     p.range_counter = ws_u32(c, c->ws.counters);
+    p.wbits = c->wbits;
+    p.wlist = c->wlist;
+    p.wn = c->wn;
     p.lut = c->lut;
     p.start = c->cfg.window_start_ms;
     p.window = (uint32_t)c->cfg.window_ms;
@@ -509,6 +516,29 @@ int sinet_classify_histogram_sortreduce(sinet_ctx* c, const sinet_records* r, vo
     }
     c->launches += (uint64_t)k;
     c->last_strategy = 3;
+    return SINET_OK;
+}
+
+size_t sinet_watchlist_bytes(uint32_t n) { return (size_t)2048 * 4 + align_up((size_t)n * 4, 256); }
+
+int sinet_set_watchlist(sinet_ctx* c, const uint32_t* ips, uint32_t n, void* d_buf, size_t buf_bytes) {
+    if (!c) return SINET_E_INVAL;
+    if (n == 0) { c->wn = 0; c->wbits = c->wlist = nullptr; return SINET_OK; }
+    if (!ips || !d_buf || buf_bytes < sinet_watchlist_bytes(n) || (reinterpret_cast<uintptr_t>(d_buf) & 15u))
+        return fail(c, SINET_E_INVAL, "watchlist: NULL list or device buffer too small / misaligned");
+    std::vector<uint32_t> list(ips, ips + n);
+    std::sort(list.begin(), list.end());
+    list.erase(std::unique(list.begin(), list.end()), list.end());   // set semantics
+    std::vector<uint32_t> bits(2048, 0u);
+    for (uint32_t a : list) bits[a >> 21] |= 1u << ((a >> 16) & 31u);
+    DeviceGuard dg(c->device);
+    unsigned char* b = static_cast<unsigned char*>(d_buf);
+    SINET_CUDA(c, cudaMemcpyAsync(b, bits.data(), 2048 * 4, cudaMemcpyHostToDevice, c->stream));
+    SINET_CUDA(c, cudaMemcpyAsync(b + 2048 * 4, list.data(), list.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->wbits = reinterpret_cast<const uint32_t*>(b);
+    c->wlist = reinterpret_cast<const uint32_t*>(b + 2048 * 4);
+    c->wn = (uint32_t)list.size();
     return SINET_OK;
 }
 

@@ -46,6 +46,25 @@ __device__ __forceinline__ uint32_t member(uint32_t ip, const Table& T) {
     return cnt & 1u;
 }
 
+// ---------------------------------------------------------------- NEXT-2: watchlist predicate
+// Exact-address set (AbuseIPDB / GRIZZLY STEPPE lists): a /16 bitmap
+// rejects most addresses with one cached load, a binary search confirms the rest.
+__device__ __forceinline__ bool watched(uint32_t ip, const KernelParams& p) {
+    if (!((__ldg(p.wbits + (ip >> 21)) >> ((ip >> 16) & 31u)) & 1u)) return false;
+    uint32_t lo = 0, len = p.wn;
+    while (len) {
+        const uint32_t half = len >> 1;
+        if (__ldg(p.wlist + lo + half) < ip) { lo += half + 1; len -= half + 1; }
+        else len = half;
+    }
+    return lo < p.wn && __ldg(p.wlist + lo) == ip;
+}
+
+// a record passes the filter iff there is no watchlist or an endpoint is listed
+__device__ __forceinline__ bool watch_pass(uint32_t src, uint32_t dst, const KernelParams& p) {
+    return p.wn == 0u || watched(src, p) || watched(dst, p);
+}
+
 // ---------------------------------------------------------------- a5: Map to a ms bin
 // key = (ts - start) / w for start <= ts < start + W (bins of 1 ms P:L217,
 // half-open, reading A15).  d < W < 2^32, so a 32-bit quotient with one

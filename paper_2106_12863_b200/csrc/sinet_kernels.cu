@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
         uint32_t tag4 = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const bool valid = vvalid(p, base + j);
+            const bool valid = vvalid(p, base + j) && watch_pass(r.src[j], r.dst[j], p);
             const uint32_t s_in = member(r.src[j], T);
             const uint32_t d_in = member(r.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;

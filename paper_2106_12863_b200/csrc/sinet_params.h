@@ -42,6 +42,9 @@ struct KernelParams {
     uint32_t ranges_per_group;     // 0 = default: record ranges handed out per group (load balance)
     uint32_t n_ranges;             // set by the launcher
     uint32_t* range_counter;       // zeroed by the launcher before each launch
+    const uint32_t* wbits;         // NEXT-2 watchlist: [2048] bitmap of /16 blocks holding a listed address
+    const uint32_t* wlist;         // sorted distinct listed addresses
+    uint32_t wn;                   // 0 = no watchlist
     uint32_t lut;                  // 4 x 2 bits, index s_in*2+d_in
     uint64_t start;                // window start (ms)
     uint32_t window;               // W (ms) < 2^32

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
         load4(p, base, r);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const bool valid = vvalid(p, base + j);
+            const bool valid = vvalid(p, base + j) && watch_pass(r.src[j], r.dst[j], p);
             const uint32_t s_in = member(r.src[j], T);
             const uint32_t d_in = member(r.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;

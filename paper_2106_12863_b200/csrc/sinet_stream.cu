@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         uint32_t tag4 = 0, bmin = 0xFFFFFFFFu, bmax = 0u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const bool valid = full || (have && vvalid(p, my_g * 4 + j));
+            const bool valid = (full || (have && vvalid(p, my_g * 4 + j))) && watch_pass(cur.src[j], cur.dst[j], p);
             const uint32_t s_in = member(cur.src[j], T);
             const uint32_t d_in = member(cur.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;

@@ -149,6 +149,19 @@ class SinetHistogram:
               self.ctx, "classify_sortreduce")
         return scratch
 
+    def set_watchlist(self, ips):
+        """NEXT-2: count only records with a listed source or destination (None/[] removes it)."""
+        ips = np.ascontiguousarray(np.asarray([] if ips is None else ips, dtype=np.uint32))
+        n = len(ips)
+        if n == 0:
+            check(lib.sinet_set_watchlist(self.ctx, None, 0, None, 0), self.ctx, "set_watchlist")
+            self._watch = None
+            return
+        need = lib.sinet_watchlist_bytes(n)
+        self._watch = torch.empty(need, dtype=torch.uint8, device=self.device)
+        check(lib.sinet_set_watchlist(self.ctx, ips.ctypes.data_as(ctypes.c_void_p), n, _ptr(self._watch), need),
+              self.ctx, "set_watchlist")
+
     def finalize(self):
         check(lib.sinet_finalize(self.ctx), self.ctx, "finalize")
 

@@ -331,3 +331,31 @@ def test_nccl_reduce_single_rank(S, oracle_lib):
     assert h.owned_range() == (0, wl.nbins)
     np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
     np.testing.assert_array_equal(h.read_totals(), o.totals)
+
+
+# ----------------------------------------------------------------------------- NEXT-2 watchlist
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_watchlist_parity(S, oracle_lib, strategy):
+    """Filter by an exact-IP watchlist (either endpoint), then histogram, vs the oracle."""
+    wl = WORKLOADS["c1"].with_(n=400_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    rng = np.random.default_rng(300)
+    listed = np.concatenate([rng.choice(cols[1], 150), rng.choice(cols[2], 150),
+                             rng.integers(0, 1 << 32, 577, dtype=np.uint64).astype(np.uint32)])
+    o = oracle_lib.classify_histogram_watched(*cols, nets, lens, listed, wl.window_start_ms, wl.window_ms, 1)
+    for sr in (False, True):
+        h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, order=strategy)
+        h.set_watchlist(listed)
+        d = dev_cols(cols)
+        if sr:
+            h.classify_sortreduce(*d)
+        else:
+            h.classify(*d)
+        np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count)
+        np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
+        np.testing.assert_array_equal(h.read_totals(), o.totals)
+        h.set_watchlist(None)   # removing the filter restores the full histogram
+        h.reset()
+        h.classify(*d)
+        assert int(h.read_totals()[:4].sum()) == wl.n

@@ -318,3 +318,49 @@ def test_sparse_export_matches_definition(oracle_lib):
     # sparse bound and conservation
     assert len(t) <= min(wl.n, wl.nbins) and int(cc.sum()) == int(res.count[0].sum())
     assert np.all(np.diff(t.astype(np.int64)) > 0)
+
+
+# ----------------------------------------------------------------------------- NEXT-2 watchlist
+def test_watch_filter_worked_values(oracle_lib):
+    # empty list -> empty output; destination listed, source not -> retained
+    src = np.array([ip("1.2.3.4"), ip("5.6.7.8"), ip("9.9.9.9")], np.uint32)
+    dst = np.array([ip("8.8.8.8"), ip("1.2.3.4"), ip("7.7.7.7")], np.uint32)
+    assert oracle_lib.watch_filter(src, dst, []).tolist() == []
+    assert oracle_lib.watch_filter(src, dst, [ip("1.2.3.4")]).tolist() == [0, 1]
+    assert oracle_lib.watch_filter(src, dst, [ip("7.7.7.7"), ip("7.7.7.7")]).tolist() == [2]   # set semantics
+
+
+def test_watch_filter_vs_python_set_and_properties(oracle_lib):
+    # 1000 synthetic records, exactly 10 touching listed IPs -> 10 kept; union
+    # superset and idempotence; filter-then-histogram conservation
+    rng = np.random.default_rng(877)
+    listed = rng.choice(np.arange(200, 2_000_000, dtype=np.uint32), 877, replace=False)
+    src = rng.integers(3_000_000, 1 << 32, 1000, dtype=np.uint64).astype(np.uint32)
+    dst = rng.integers(3_000_000, 1 << 32, 1000, dtype=np.uint64).astype(np.uint32)
+    hit = rng.choice(1000, 10, replace=False)
+    for k, r in enumerate(hit):
+        (src if k % 2 else dst)[r] = listed[k]
+    keep = oracle_lib.watch_filter(src, dst, listed)
+    assert sorted(keep.tolist()) == sorted(hit.tolist())
+    lset = set(int(x) for x in listed[:400])
+    ref = [i for i in range(1000) if int(src[i]) in lset or int(dst[i]) in lset]
+    assert oracle_lib.watch_filter(src, dst, listed[:400]).tolist() == ref
+    a = set(oracle_lib.watch_filter(src, dst, listed[:300]).tolist())
+    assert a <= set(keep.tolist())
+    k2 = oracle_lib.watch_filter(src[keep], dst[keep], listed)
+    assert k2.tolist() == list(range(len(keep)))
+
+
+def test_watched_histogram_equals_histogram_of_filtered(oracle_lib):
+    wl, nets, lens, rec = _c1_small(100_000)
+    ts, src, dst, nb = to_numpy(rec)
+    listed = np.unique(np.concatenate([src[:150], dst[1000:1150]]))
+    res = oracle_lib.classify_histogram_watched(ts, src, dst, nb, nets, lens, listed, wl.window_start_ms,
+                                                wl.window_ms, 1)
+    lset = set(int(x) for x in listed)
+    m = np.array([int(s) in lset or int(d) in lset for s, d in zip(src, dst)])
+    ref = oracle_lib.classify_histogram(ts[m], src[m], dst[m], nb[m], nets, lens, wl.window_start_ms,
+                                        wl.window_ms, 1)
+    np.testing.assert_array_equal(res.count, ref.count)
+    np.testing.assert_array_equal(res.totals, ref.totals)
+    assert int(res.m_count.sum()) == int(m.sum())
