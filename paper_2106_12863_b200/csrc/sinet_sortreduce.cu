@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
         load4(p, base, r);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const bool valid = vvalid(p, base + j) && watch_pass(r.src[j], r.dst[j], p);
+            const bool inrange = vvalid(p, base + j);
+            const bool valid = inrange && watch_pass(r.src[j], r.dst[j], p);
             const uint32_t s_in = member(r.src[j], T);
             const uint32_t d_in = member(r.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
             uint32_t bin = 0;
             const bool inw = map_bin(r.ts[j], p, bin);
             const bool directed = valid && dir < 2u;
-            if (valid) {
+            if (inrange) {   // every record gets a key: filtered or unbinned ones the sentinel
                 const uint64_t a = base + j - p.head;
                 keys[a] = (directed && inw) ? bin * 2u + dir : sentinel;
                 vals[a] = r.by[j];

@@ -495,7 +495,7 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     const bool w1 = p.width == 1u;
     const int g = stream_groups_for(p);
     KernelParams q = p;   // ranges: a few per group, each at least a few chunks long
-    const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 3u);
+    const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 4u);
     const uint64_t max_r = p.nv / (4u * kStreamThreads * 4u) + 1u;
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
 #define LAUNCH(G, S)                                                                                \
