@@ -134,6 +134,7 @@ struct sinet_ctx {
     bool agg = false;             // warp aggregation of equal keys in the stream kernel (measured slower on C4)
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t ranges_per_group = 0;
+    uint32_t stream_threads = 0;
     // NEXT-2 watchlist (caller-owned device buffer)
     const uint32_t* wbits = nullptr;
     const uint32_t* wlist = nullptr;
@@ -199,6 +200,7 @@ KernelParams base_params(sinet_ctx* c) {
     p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
     p.stream_groups = c->stream_groups;
     p.ranges_per_group = c->ranges_per_group;
+    p.stream_threads = c->stream_threads;
     p.range_counter = ws_u32(c, c->ws.counters);
     p.wbits = c->wbits;
     p.wlist = c->wlist;
@@ -380,6 +382,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     if (const char* a = std::getenv("SINET_AGG")) c->agg = std::atoi(a) != 0;
     if (const char* g = std::getenv("SINET_STREAM_GROUPS")) c->stream_groups = (uint32_t)std::atoi(g);
     if (const char* r = std::getenv("SINET_RANGES")) c->ranges_per_group = (uint32_t)std::atoi(r);
+    if (const char* t = std::getenv("SINET_STREAM_THREADS")) c->stream_threads = (uint32_t)std::atoi(t);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states

@@ -186,6 +186,42 @@ __device__ __forceinline__ void load4(const KernelParams& p, uint64_t vbase, Rec
     }
 }
 
+// Two consecutive records at even virtual index vbase (RPT = 2 configuration).
+struct Rec2 {
+    uint64_t ts[2];
+    uint32_t src[2], dst[2];
+    uint64_t by[2];
+};
+
+__device__ __forceinline__ void load2(const KernelParams& p, uint64_t vbase, Rec2& r) {
+    if (vbase >= p.head && vbase + 2 <= p.nv) {
+        const uint64_t a = vbase - p.head;
+        const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(p.ts + a));
+        const uint2 s = __ldcs(reinterpret_cast<const uint2*>(p.src + a));
+        const uint2 d = __ldcs(reinterpret_cast<const uint2*>(p.dst + a));
+        const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(p.bytes + a));
+        r.ts[0] = t.x; r.ts[1] = t.y; r.src[0] = s.x; r.src[1] = s.y;
+        r.dst[0] = d.x; r.dst[1] = d.y; r.by[0] = b.x; r.by[1] = b.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const bool ok = vvalid(p, vbase + j);
+            const uint64_t a = vbase + j - p.head;
+            r.ts[j] = ok ? p.ts[a] : 0ull;
+            r.src[j] = ok ? p.src[a] : 0u;
+            r.dst[j] = ok ? p.dst[a] : 0u;
+            r.by[j] = ok ? p.bytes[a] : 0ull;
+        }
+    }
+}
+
+template <int R> struct RecN;
+template <> struct RecN<4> { using T = Rec4; };
+template <> struct RecN<2> { using T = Rec2; };
+template <int R> __device__ __forceinline__ void loadN(const KernelParams& p, uint64_t vbase, typename RecN<R>::T& r);
+template <> __device__ __forceinline__ void loadN<4>(const KernelParams& p, uint64_t vbase, Rec4& r) { load4(p, vbase, r); }
+template <> __device__ __forceinline__ void loadN<2>(const KernelParams& p, uint64_t vbase, Rec2& r) { load2(p, vbase, r); }
+
 __device__ __forceinline__ void store_tags4(const KernelParams& p, uint64_t vbase, uint32_t tag4) {
     if (p.tags_vec && vbase >= p.head && vbase + 4 <= p.nv) {
         *reinterpret_cast<uint32_t*>(p.tags + (vbase - p.head)) = tag4;

@@ -9,7 +9,7 @@ constexpr uint32_t kTileBins = 256;        // bins per claim tile (8 KB of u64[4
 constexpr uint32_t kClsWords = 4096;       // 65536 /16 blocks x 2 bits
 constexpr uint32_t kRankWords = 2048;      // 4096 u16 prefix counts
 // staged beyond the class table + rank (24 KB): level 2 + entries + boundaries if they fit here
-constexpr uint32_t kSmallExtraBytes = 9 * 1024;
+constexpr uint32_t kSmallExtraBytes = 7 * 1024;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // tile state word: epoch << 2 | state
@@ -39,6 +39,7 @@ struct KernelParams {
     uint32_t n_mixed;
     uint32_t small;                // 1: level 2, entries and boundaries fit in shared memory
     uint32_t stream_groups;        // 0 auto, 1 or 2: layout of the stream kernel's ring
+    uint32_t stream_threads;       // 0 auto, 512 or 1024: stream kernel block size
     uint32_t ranges_per_group;     // 0 = default: record ranges handed out per group (load balance)
     uint32_t n_ranges;             // set by the launcher
     uint32_t* range_counter;       // zeroed by the launcher before each launch

@@ -127,8 +127,12 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
 // classified, and the tiles are retired (stored or added) right after.  A CTA
 // never waits on another CTA's tile while it holds an unreleased claim, so
 // the protocol cannot deadlock.
-template <int THREADS, int NG, int WS, bool kAgg, bool kW1, bool kSmall>
+template <int THREADS, int NG, int WS, int RPT, bool kAgg, bool kW1, bool kSmall>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
+    // RPT records per thread per chunk; with RPT == 2 the side totals live in shared
+    // memory per warp (registers for 1024 threads)
+    constexpr bool kSmemTot = (RPT == 2);
+    using Rec = typename RecN<RPT>::T;
     constexpr int GT = THREADS / NG;          // threads per group
     constexpr int NW = THREADS / 32;
     constexpr int GW = GT / 32;               // warps per group
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_red_all[NG][2][2][GW];
     __shared__ uint32_t s_state_all[NG][NT];   // (t+1) << 2 | claim outcome, per group
-    __shared__ unsigned long long s_tot[NW * 12];
+    __shared__ unsigned long long s_tot[(RPT == 2) ? 1 : NW * 12];
 
     // NG independent groups per CTA, each with its own ring and half of the CTA's records;
     // the lookup table is shared.  A group synchronises on its own named barrier.
@@ -302,6 +306,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     const uint64_t ngroups = (p.nv + 3) / 4;
     const uint64_t nranges = (uint64_t)p.n_ranges;
     __shared__ uint64_t s_range[NG];
+    __shared__ unsigned long long s_wtot[kSmemTot ? NW : 1][12];   // per-warp totals (RPT == 2)
+    if (kSmemTot) {
+        for (uint32_t i = threadIdx.x; i < (uint32_t)NW * 12u; i += THREADS) (&s_wtot[0][0])[i] = 0ull;
+    }
     WarpTotals tot;
     tot.zero();
     for (;;) {
@@ -309,31 +317,36 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     group_sync();
     const uint64_t range = s_range[gid];
     if (range >= nranges) break;
-    const uint64_t g0 = ngroups * range / nranges, g1 = ngroups * (range + 1) / nranges;
+    // this range in virtual records [r0, r1) (a multiple of 4 apart)
+    const uint64_t r0 = (ngroups * range / nranges) * 4, r1 = (ngroups * (range + 1) / nranges) * 4;
     lo_t = 0; act_t = 0; have_window = false; hull_lo = 0xFFFFFFFFu; hull_hi = 0u;
 
     // chunks whose every record is valid: not the batch's ragged first/last 4-record group
-    const uint64_t full_lo = (p.head != 0u) ? 1u : 0u;
-    const uint64_t full_hi = (g1 * 4 > p.nv) ? g1 - 1 : g1;
-    Rec4 cur, nxt;
-    if (g0 + tid < g1) load4(p, (g0 + tid) * 4, cur);
+    const uint64_t full_lo = (p.head != 0u) ? 4u : 0u;
+    const uint64_t full_hi = (r1 > p.nv) ? r1 - 4 : r1;
+    constexpr uint64_t CH = (uint64_t)GT * RPT;   // records per chunk
+    Rec cur, nxt;
+    if (r0 + (uint64_t)tid * RPT < r1) loadN<RPT>(p, r0 + (uint64_t)tid * RPT, cur);
     uint32_t parity = 0;
 
-    for (uint64_t cbase = g0; cbase < g1; cbase += GT, parity ^= 1u) {
-        const uint64_t my_g = cbase + tid;
-        const bool have = my_g < g1;
-        // every record of the chunk valid (all but the CTA's ragged ends): no per-record checks
-        const bool full = cbase >= full_lo && cbase + GT <= full_hi;
+    for (uint64_t cbase = r0; cbase < r1; cbase += CH, parity ^= 1u) {
+        const uint64_t my_v = cbase + (uint64_t)tid * RPT;   // this thread's first record
+        const bool have = my_v < r1;
+        // every record of the chunk valid (all but the batch's ragged ends): no per-record checks
+        const bool full = cbase >= full_lo && cbase + CH <= full_hi;
         const bool tags_on = p.tags != nullptr;
-        if (cbase + GT + tid < g1) load4(p, (cbase + GT + tid) * 4, nxt);   // prefetch
+        if (my_v + CH < r1) loadN<RPT>(p, my_v + CH, nxt);   // prefetch
 
         // ---- a3-a5: classify and map this chunk (the claims issued last chunk resolve meanwhile)
-        uint32_t bin4[4], dir4[4];
-        bool binned4[4];
+        uint32_t bin4[RPT], dir4[RPT];
+        bool binned4[RPT];
         uint32_t tag4 = 0, bmin = 0xFFFFFFFFu, bmax = 0u;
+        WarpTotals ctot;   // this chunk's records (RPT == 2: reduced into shared memory below)
+        if (kSmemTot) ctot.zero();
+        WarpTotals& tt = kSmemTot ? ctot : tot;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const bool valid = (full || (have && vvalid(p, my_g * 4 + j))) && watch_pass(cur.src[j], cur.dst[j], p);
+        for (int j = 0; j < RPT; ++j) {
+            const bool valid = (full || (have && vvalid(p, my_v + j))) && watch_pass(cur.src[j], cur.dst[j], p);
             const uint32_t s_in = member(cur.src[j], T);
             const uint32_t d_in = member(cur.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
@@ -353,9 +366,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             dir4[j] = dir;
             if (binned4[j]) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
             if (tags_on) tag4 |= (s_in | (d_in << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
-            tot.add(valid, cell, directed && !inw, dir, cur.by[j]);
+            tt.add(valid, cell, directed && !inw, dir, cur.by[j]);
         }
-        if (tags_on && have) store_tags4(p, my_g * 4, tag4);
+        if (tags_on && have) {
+            if (RPT == 4) store_tags4(p, my_v, tag4);
+            else for (int j = 0; j < RPT; ++j) if (vvalid(p, my_v + j)) p.tags[my_v + j - p.head] = (uint8_t)(tag4 >> (8 * j));
+        }
+        if (kSmemTot) {   // warp-reduce this chunk's totals into the warp's shared slots
+            const unsigned long long cT = __reduce_add_sync(kFull, ctot.cT), cS = __reduce_add_sync(kFull, ctot.cS);
+            const unsigned long long cD = __reduce_add_sync(kFull, ctot.cD), cSD = __reduce_add_sync(kFull, ctot.cSD);
+            const unsigned long long bT = warp_sum_u64(ctot.bT), bS = warp_sum_u64(ctot.bS);
+            const unsigned long long bD = warp_sum_u64(ctot.bD), bSD = warp_sum_u64(ctot.bSD);
+            unsigned long long o[4] = {0ull, 0ull, 0ull, 0ull};
+            if (__any_sync(kFull, (ctot.oc[0] | ctot.oc[1]) != 0u)) {
+                o[0] = __reduce_add_sync(kFull, ctot.oc[0]); o[1] = __reduce_add_sync(kFull, ctot.oc[1]);
+                o[2] = warp_sum_u64(ctot.ob[0]); o[3] = warp_sum_u64(ctot.ob[1]);
+            }
+            if (lane == 0) {
+                const uint32_t w = threadIdx.x >> 5;
+                s_wtot[w][0] += cT - cS - cD + cSD; s_wtot[w][1] += cD - cSD; s_wtot[w][2] += cS - cSD; s_wtot[w][3] += cSD;
+                s_wtot[w][4] += bT - bS - bD + bSD; s_wtot[w][5] += bD - bSD; s_wtot[w][6] += bS - bSD; s_wtot[w][7] += bSD;
+                s_wtot[w][8] += o[0]; s_wtot[w][9] += o[1]; s_wtot[w][10] += o[2]; s_wtot[w][11] += o[3];
+            }
+        }
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
         if (lane == 0) { s_red[parity][0][warp] = bmin; s_red[parity][1][warp] = bmax; }
@@ -390,14 +423,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 
         // ---- a6 (accumulate): reduce the chunk into the ring
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RPT; ++j) {
             const bool b = binned4[j];
             bool act = b;
             uint32_t cnt = 1u;
             uint64_t byt = cur.by[j];
             // warp aggregation of equal (bin, dir) keys (hot bins, bursts): only when a
             // cheap neighbour test finds a duplicate in the warp (records of one slot are
-            // 4 apart in stream order, so hot keys show up in adjacent lanes)
+            // RPT apart in stream order, so hot keys show up in adjacent lanes)
             bool try_agg = false;
             if (kAgg) {
                 const uint32_t k32 = b ? ((bin4[j] << 1) | dir4[j]) : 0xFFFFFFFFu - lane;
@@ -453,29 +486,39 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     }
     }   // ranges
     __syncthreads();
-    flush_totals(tot, p.totals, s_tot);
+    if (kSmemTot) {
+        if (threadIdx.x < 12) {
+            unsigned long long acc = 0;
+            for (int w = 0; w < NW; ++w) acc += s_wtot[w][threadIdx.x];
+            if (acc) atomicAdd(p.totals + threadIdx.x, acc);
+        }
+    } else {
+        flush_totals(tot, p.totals, s_tot);
+    }
 }
 
 // ---------------------------------------------------------------- launch
 namespace {
-constexpr int kStreamThreads = 512;
-// two layouts of the same 192 KB of ring: one group with an 8192-bin ring (sparse input:
-// a 2048-record chunk spans many ms) or two independent groups with 4096-bin rings
-// (dense input: one group's barrier/retire phase overlaps the other's loads and lookups)
+// ring layouts of the same 192 KB: one group with an 8192-bin ring (sparse input: a
+// chunk spans many ms) or two independent groups with 4096-bin rings (dense input:
+// one group's barrier/retire phase overlaps the other's loads and lookups)
 constexpr int kRingBins1 = 8192;
 constexpr int kRingBins2 = 4096;
 }  // namespace
 
-#define SINET_STREAM_KERNEL(G, A, W, S) k_hist_stream<kStreamThreads, G, (G == 1 ? kRingBins1 : kRingBins2), A, W, S>
+// (threads, groups, records per thread): 512/1/4, 512/2/4, 1024/1/2, 1024/2/2
+#define SINET_STREAM_KERNEL(TH, G, A, W, S) \
+    k_hist_stream<TH, G, (G == 1 ? kRingBins1 : kRingBins2), (TH == 512 ? 4 : 2), A, W, S>
 
 cudaError_t setup_hist_stream() {
     const int mx = (int)((size_t)kRingBins1 * 6u * 4u + kMaxTableSmem);
     cudaError_t e;
-#define SET(G, A, W, S)                                                                                 \
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W, S), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
+#define SET(TH, G, A, W, S)                                                                                 \
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(TH, G, A, W, S), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
-#define SET4(G, S) SET(G, true, true, S) SET(G, true, false, S) SET(G, false, true, S) SET(G, false, false, S)
-    SET4(1, true) SET4(1, false) SET4(2, true) SET4(2, false)
+#define SET4(TH, G, S) SET(TH, G, true, true, S) SET(TH, G, true, false, S) SET(TH, G, false, true, S) SET(TH, G, false, false, S)
+    SET4(512, 1, true) SET4(512, 1, false) SET4(512, 2, true) SET4(512, 2, false)
+    SET4(1024, 1, true) SET4(1024, 1, false) SET4(1024, 2, true) SET4(1024, 2, false)
 #undef SET4
 #undef SET
     return cudaSuccess;
@@ -490,23 +533,26 @@ int stream_groups_for(const KernelParams& p) {
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st) {
     static_assert(kRingBins1 == 2 * kRingBins2, "both layouts use the same shared memory");
     const size_t sm = (size_t)kRingBins1 * 6u * 4u + table_smem_bytes(p.nbnd, p.n_mixed, p.small);
-    const uint64_t chunks = (p.nv / 4 + kStreamThreads - 1) / kStreamThreads;
+    const int th = (p.stream_threads == 1024) ? 1024 : 512;
+    const uint64_t chunks = (p.nv / 4 + 511) / 512;
     const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
     const bool w1 = p.width == 1u;
     const int g = stream_groups_for(p);
     KernelParams q = p;   // ranges: a few per group, each at least a few chunks long
     const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 4u);
-    const uint64_t max_r = p.nv / (4u * kStreamThreads * 4u) + 1u;
+    const uint64_t max_r = p.nv / (4u * 512u * 4u) + 1u;
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
-#define LAUNCH(G, S)                                                                                \
-    if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S)<<<grid, kStreamThreads, sm, st>>>(q);       \
-    else if (agg) SINET_STREAM_KERNEL(G, true, false, S)<<<grid, kStreamThreads, sm, st>>>(q);       \
-    else if (w1) SINET_STREAM_KERNEL(G, false, true, S)<<<grid, kStreamThreads, sm, st>>>(q);        \
-    else SINET_STREAM_KERNEL(G, false, false, S)<<<grid, kStreamThreads, sm, st>>>(q);
     cudaError_t e = cudaMemsetAsync(p.range_counter, 0, 8, st);
     if (e != cudaSuccess) return e;
-    if (g == 2) { if (p.small) { LAUNCH(2, true) } else { LAUNCH(2, false) } }
-    else { if (p.small) { LAUNCH(1, true) } else { LAUNCH(1, false) } }
+#define LAUNCH(TH, G, S)                                                                                \
+    if (agg && w1) SINET_STREAM_KERNEL(TH, G, true, true, S)<<<grid, TH, sm, st>>>(q);                  \
+    else if (agg) SINET_STREAM_KERNEL(TH, G, true, false, S)<<<grid, TH, sm, st>>>(q);                  \
+    else if (w1) SINET_STREAM_KERNEL(TH, G, false, true, S)<<<grid, TH, sm, st>>>(q);                   \
+    else SINET_STREAM_KERNEL(TH, G, false, false, S)<<<grid, TH, sm, st>>>(q);
+#define LAUNCH_G(TH, S) if (g == 2) { LAUNCH(TH, 2, S) } else { LAUNCH(TH, 1, S) }
+    if (th == 1024) { if (p.small) { LAUNCH_G(1024, true) } else { LAUNCH_G(1024, false) } }
+    else { if (p.small) { LAUNCH_G(512, true) } else { LAUNCH_G(512, false) } }
+#undef LAUNCH_G
 #undef LAUNCH
     return cudaGetLastError();
 }
