@@ -78,6 +78,8 @@ def describe(wl, world, strategy):
                      + (f", {world} contiguous shards (weak scaling, {wl.n // world:,}/GPU)" if world > 1 else "")),
         "records": wl.n, "records_per_gpu": wl.n // world, "bins": wl.nbins, "prefixes": wl.n_prefixes,
         "order": wl.order, "strategy": strategy, "parallelism": f"dp{world}",
+        "exchange": ("none (1 GPU)" if world == 1 else
+                     "NCCL: all-gather touched ranges + send/recv of overlaps (sparse) or reduce-scatter (dense)"),
         "l2": "no flush: inputs (24 B/record) and bins (32 B/bin) are each larger than the 126 MB L2",
     }
 
@@ -278,6 +280,7 @@ def run_ours(args):
     else:
         kern_avg = kern_ms_total / max(kern_n, 1)
     strat_used = {1: "stream", 2: "shuffled"}.get(h.last_strategy, str(h.last_strategy))
+    exch_used = {0: None, 1: "dense", 2: "sparse"}.get(h.last_exchange)
 
     # ---- correctness gate (properties at full size + sampled bins vs the oracle)
     gate = None if args.profile else check_result(S, h, wl, ts, src, dst, nb, nets, lens, rank, world, dev)
@@ -319,7 +322,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": describe(wl, world, strat_used),
+            "config": dict(describe(wl, world, strat_used), exchange_used=exch_used),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": bw, "unit": "GB/s",
                          "frac": achieved / bw, "traffic": ncu_traffic(wl.name, strat_used),
                          "kernel": "k_hist_stream" if strat_used == "stream" else "k_hist_atomic",

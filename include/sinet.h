@@ -200,8 +200,28 @@ int sinet_nccl_unique_id(void* out128);
  * then an in-place reduce-scatter (u64 sum) leaves rank g the global sums of
  * bins [g*B_pad/world, (g+1)*B_pad/world); totals are all-reduced so every
  * rank holds the global totals.  world == 1 without a communicator: finalize only.
+ * With contiguous time shards each rank's partial histogram is zero outside the
+ * bins it touched, so by default (exchange mode 0) the ranks all-gather their
+ * touched ranges and, when that moves at most half the data of the dense
+ * reduce-scatter, only the overlaps travel (grouped ncclSend/ncclRecv into the
+ * workspace's staging, then added to the owned bins) -- same result.
+ * Synchronises the stream in that case (the plan is made on the host).
  * Errors: E_STATE (already reduced), E_NCCL (no comm / NCCL failure). */
 int sinet_reduce(sinet_ctx* ctx);
+
+/* Merge strategy for sinet_reduce: 0 automatic, 1 dense reduce-scatter,
+ * 2 sparse touched-range exchange (falls back to dense if staging is too small).
+ * sinet_last_exchange reports what the last reduce did (1 dense, 2 sparse, 0 none). */
+int sinet_set_exchange(sinet_ctx* ctx, int mode);
+int sinet_last_exchange(const sinet_ctx* ctx);
+/* Smallest / largest bin written since the last reset (min > max: none); synchronises. */
+int sinet_touched_range(sinet_ctx* ctx, uint32_t* min_bin, uint32_t* max_bin);
+/* Host-side plan of the sparse exchange (no GPU): touched[2*r], touched[2*r+1] =
+ * min / max bin rank r wrote (min > max: none).  Fills send[2*o] = first bin,
+ * send[2*o+1] = count this rank sends to owner o, and recv[2*r], recv[2*r+1] what
+ * it receives from rank r.  Errors: E_INVAL. */
+int sinet_exchange_plan(int32_t world, int32_t rank, uint64_t nbins, uint64_t nbins_pad, const uint32_t* touched,
+                        uint64_t* send, uint64_t* recv);
 
 /* Owned bin range: [0, B) before reduce or with world == 1, else this rank's
  * slice clipped to [0, B). */

@@ -11,6 +11,8 @@ from ._native import (  # noqa: F401
     DIR_IN, DIR_NEITHER, DIR_OUT, LUT_ALG1, LUT_SRC_PRIORITY, LUT_STRICT, METRIC_BYTES,
     METRIC_COUNT, ORDER_AUTO, ORDER_SHUFFLED, ORDER_STREAM, SinetError,
 )
-from .histogram import SinetHistogram, owned_bin_range, padded_bins, shard_range, table_member_host  # noqa: F401
+from .histogram import (  # noqa: F401
+    SinetHistogram, exchange_plan, owned_bin_range, padded_bins, shard_range, table_member_host,
+)
 
 __version__ = "0.1.0"

@@ -79,6 +79,10 @@ _SIGS = {
     "sinet_set_tuning": ([_vp, _i, _i], _i),
     "sinet_watchlist_bytes": ([_u32], ctypes.c_size_t),
     "sinet_set_watchlist": ([_vp, _vp, _u32, _vp, ctypes.c_size_t], _i),
+    "sinet_set_exchange": ([_vp, _i], _i),
+    "sinet_last_exchange": ([_vp], _i),
+    "sinet_touched_range": ([_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u32)], _i),
+    "sinet_exchange_plan": ([ctypes.c_int32, ctypes.c_int32, _u64, _u64, _vp, _vp, _vp], _i),
     "sinet_table_member_host": ([_vp, _vp, _u32, _vp, _u64, _vp], _i),
 }
 for _name, (_args, _res) in _SIGS.items():

@@ -26,6 +26,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
 constexpr int kNcclSum = 0;
+constexpr int kNcclUint32 = 3;
 constexpr int kNcclUint64 = 5;
 
 struct NcclApi {
@@ -35,6 +36,9 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -55,6 +59,9 @@ NcclApi* nccl_api(std::string* err) {
     SINET_SYM(CommDestroy, "ncclCommDestroy")
     SINET_SYM(ReduceScatter, "ncclReduceScatter")
     SINET_SYM(AllReduce, "ncclAllReduce")
+    SINET_SYM(AllGather, "ncclAllGather")
+    SINET_SYM(Send, "ncclSend")
+    SINET_SYM(Recv, "ncclRecv")
     SINET_SYM(GroupStart, "ncclGroupStart")
     SINET_SYM(GroupEnd, "ncclGroupEnd")
     SINET_SYM(GetErrorString, "ncclGetErrorString")
@@ -90,10 +97,19 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, rank, mentry, l2, flags, sparse, counters, total;
+    size_t totals, cls2, entry, bnd, rank, mentry, l2, flags, sparse, counters, xranges, staging, staging_bytes, total;
 };
 
-WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
+// Device staging for the sparse multi-GPU exchange: a quarter of the owned slice, capped.
+size_t exchange_staging_bytes(uint64_t n_tiles, int world) {
+    if (world <= 1) return 0;
+    const uint64_t per = n_tiles * kTileBins / (uint64_t)world;
+    uint64_t b = per * 32u / 4u;
+    const uint64_t cap = 256ull << 20;
+    return (size_t)(b < cap ? b : cap);
+}
+
+WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes, int world) {
     WsLayout L{};
     size_t off = 0;
     L.totals = off; off = align_up(off + 16 * 8, 256);
@@ -105,7 +121,10 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes) {
     L.l2 = off;     off = align_up(off + (size_t)(2u * n_prefixes + 1u) * 64, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
-    L.counters = off; off = align_up(off + 64, 256);
+    L.counters = off; off = align_up(off + 64, 256);   // [0] range counter, [4..5] touched min/max
+    L.xranges = off; off = align_up(off + (size_t)world * 8, 256);
+    L.staging_bytes = exchange_staging_bytes(n_tiles, world);
+    L.staging = off; off = align_up(off + L.staging_bytes, 256);
     L.total = off;
     return L;
 }
@@ -135,6 +154,8 @@ struct sinet_ctx {
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t ranges_per_group = 0;
     uint32_t stream_threads = 0;
+    int exchange = 0;             // multi-GPU merge: 0 auto (sparse when cheaper), 1 dense, 2 sparse
+    int last_exchange = 0;        // 1 dense reduce-scatter, 2 sparse touched-range exchange
     // NEXT-2 watchlist (caller-owned device buffer)
     const uint32_t* wbits = nullptr;
     const uint32_t* wlist = nullptr;
@@ -202,6 +223,7 @@ KernelParams base_params(sinet_ctx* c) {
     p.ranges_per_group = c->ranges_per_group;
     p.stream_threads = c->stream_threads;
     p.range_counter = ws_u32(c, c->ws.counters);
+    p.touched = ws_u32(c, c->ws.counters) + 4;
     p.wbits = c->wbits;
     p.wlist = c->wlist;
     p.wn = c->wn;
@@ -316,7 +338,45 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
 
 }  // namespace
 
+// Sparse exchange plan: rank r's partial histogram is zero outside its touched range
+// T_r = [min_r, max_r]; owner o needs T_r ∩ Own(o) from every r != o.
+struct Seg { uint64_t first, n; };
+void plan_exchange(int world, int rank, uint64_t B, uint64_t B_pad, const uint32_t* tr,
+                   std::vector<Seg>* send, std::vector<Seg>* recv) {
+    const uint64_t per = B_pad / (uint64_t)world;
+    auto own = [&](int o, uint64_t* lo, uint64_t* hi) {
+        *lo = per * (uint64_t)o; *hi = *lo + per;
+        if (*lo > B) *lo = B;
+        if (*hi > B) *hi = B;
+    };
+    auto inter = [&](int r, int o) -> Seg {
+        const uint64_t tmin = tr[2 * r], tmax = tr[2 * r + 1];
+        if (r == o || tmin > tmax) return Seg{0, 0};
+        uint64_t lo, hi;
+        own(o, &lo, &hi);
+        const uint64_t a = tmin > lo ? tmin : lo, b = (tmax + 1 < hi) ? tmax + 1 : hi;
+        return (a < b) ? Seg{a, b - a} : Seg{0, 0};
+    };
+    send->assign(world, Seg{0, 0});
+    recv->assign(world, Seg{0, 0});
+    for (int o = 0; o < world; ++o) (*send)[o] = inter(rank, o);
+    for (int r = 0; r < world; ++r) (*recv)[r] = inter(r, rank);
+}
+
 extern "C" {
+
+int sinet_exchange_plan(int32_t world, int32_t rank, uint64_t nbins, uint64_t nbins_pad, const uint32_t* touched,
+                        uint64_t* send, uint64_t* recv) {
+    if (world < 1 || rank < 0 || rank >= world || !touched || !send || !recv || nbins_pad % (uint64_t)world)
+        return SINET_E_INVAL;
+    std::vector<Seg> sd, rv;
+    plan_exchange(world, rank, nbins, nbins_pad, touched, &sd, &rv);
+    for (int k = 0; k < world; ++k) {
+        send[2 * k] = sd[k].first; send[2 * k + 1] = sd[k].n;
+        recv[2 * k] = rv[k].first; recv[2 * k + 1] = rv[k].n;
+    }
+    return SINET_OK;
+}
 
 int sinet_abi_version(void) { return SINET_ABI_VERSION; }
 uint32_t sinet_tile_bins(void) { return kTileBins; }
@@ -332,7 +392,7 @@ size_t sinet_workspace_bytes(const sinet_config* cfg, uint32_t n_prefixes) {
     std::string err;
     Geometry g;
     if (!check_cfg(cfg, &err, &g) || n_prefixes == 0 || n_prefixes > kMaxPrefixes) return 0;
-    return ws_layout(g.n_tiles, n_prefixes).total;
+    return ws_layout(g.n_tiles, n_prefixes, cfg->world).total;
 }
 
 size_t sinet_staging_bytes(uint64_t chunk_records) {
@@ -357,7 +417,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     }
     c->cfg = *cfg;
     c->geo = g;
-    c->ws = ws_layout(g.n_tiles, n_prefixes);
+    c->ws = ws_layout(g.n_tiles, n_prefixes, cfg->world);
     if (!d_bins || !d_ws || bins_bytes < (size_t)g.B_pad * 32u || ws_bytes < c->ws.total ||
         (reinterpret_cast<uintptr_t>(d_bins) & 255u) || (reinterpret_cast<uintptr_t>(d_ws) & 255u)) {
         std::fprintf(stderr, "sinet_open: bins/workspace buffer missing, too small or not 256-byte aligned\n");
@@ -383,6 +443,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     if (const char* g = std::getenv("SINET_STREAM_GROUPS")) c->stream_groups = (uint32_t)std::atoi(g);
     if (const char* r = std::getenv("SINET_RANGES")) c->ranges_per_group = (uint32_t)std::atoi(r);
     if (const char* t = std::getenv("SINET_STREAM_THREADS")) c->stream_threads = (uint32_t)std::atoi(t);
+    if (const char* x = std::getenv("SINET_EXCHANGE")) c->exchange = std::atoi(x);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
@@ -398,6 +459,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.l2, c->table.l2.data(), c->table.l2.size() * 4, cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.counters, 0, 64, c->stream));
+    OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.counters + 16, 0xFF, 4, c->stream));   // touched min = ~0
     OPEN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         OPEN_CUDA(cudaEventCreateWithFlags(&c->copy_done[k], cudaEventDisableTiming));
@@ -433,6 +495,8 @@ int sinet_reset(sinet_ctx* c) {
     if (!c) return SINET_E_INVAL;
     DeviceGuard dg(c->device);
     SINET_CUDA(c, cudaMemsetAsync(c->d_ws + c->ws.totals, 0, 16 * 8, c->stream));
+    SINET_CUDA(c, cudaMemsetAsync(c->d_ws + c->ws.counters + 16, 0xFF, 4, c->stream));   // touched min
+    SINET_CUDA(c, cudaMemsetAsync(c->d_ws + c->ws.counters + 20, 0, 4, c->stream));      // touched max
     c->epoch++;
     if (c->epoch >= (1u << 30)) {   // epoch space exhausted: re-zero the state words
         SINET_CUDA(c, cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)c->geo.n_tiles * 4, c->stream));
@@ -587,17 +651,82 @@ int sinet_reduce(sinet_ctx* c) {
         if (!c->comm) return fail(c, SINET_E_NCCL, "no communicator: call sinet_comm_init");
         NcclApi* api = nccl_api(&c->err);
         if (!api) return SINET_E_NCCL;
-        const size_t slice = (size_t)(c->geo.B_pad / (uint64_t)c->cfg.world) * 4u;   // u64 per rank
+        const int world = c->cfg.world, rank = c->cfg.rank;
+        const size_t slice = (size_t)(c->geo.B_pad / (uint64_t)world) * 4u;   // u64 per rank
         unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.totals);
+        bool sparse = false;
+        std::vector<Seg> sd, rv;
+        if (world > 1 && c->exchange != 1 && c->ws.staging_bytes) {
+            // every rank's touched range, then the same plan (and decision) on every rank
+            uint32_t* xr = ws_u32(c, c->ws.xranges);
+            ncclResult_t r = api->AllGather(ws_u32(c, c->ws.counters) + 4, xr, 2, kNcclUint32, c->comm, c->stream);
+            if (r != 0) return fail(c, SINET_E_NCCL, std::string("NCCL all-gather: ") + api->GetErrorString(r));
+            std::vector<uint32_t> h((size_t)world * 2);
+            SINET_CUDA(c, cudaMemcpyAsync(h.data(), xr, h.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+            SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+            uint64_t worst_recv = 0, total_moved = 0;
+            for (int o = 0; o < world; ++o) {
+                std::vector<Seg> s_o, r_o;
+                plan_exchange(world, o, c->geo.B, c->geo.B_pad, h.data(), &s_o, &r_o);
+                uint64_t rb = 0;
+                for (auto& g : r_o) rb += g.n;
+                total_moved += rb;
+                if (rb > worst_recv) worst_recv = rb;
+            }
+            const uint64_t dense_moved = (uint64_t)(world - 1) * (c->geo.B_pad / (uint64_t)world) * (uint64_t)world;
+            sparse = (c->exchange == 2 || total_moved * 2 <= dense_moved) &&
+                     worst_recv * 32u <= (uint64_t)c->ws.staging_bytes;
+            if (sparse) plan_exchange(world, rank, c->geo.B, c->geo.B_pad, h.data(), &sd, &rv);
+        }
         ncclResult_t r = api->GroupStart();
-        if (r == 0) r = api->ReduceScatter(c->bins, c->bins + slice * (size_t)c->cfg.rank, slice,
-                                           kNcclUint64, kNcclSum, c->comm, c->stream);
+        if (sparse) {
+            // only the touched overlaps travel: send my partial bins inside each owner's range,
+            // receive the other ranks' partial bins of my owned range into staging
+            unsigned long long* stage = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.staging);
+            size_t off = 0;
+            for (int o = 0; o < world && r == 0; ++o)
+                if (sd[o].n) r = api->Send(c->bins + sd[o].first * 4u, sd[o].n * 4u, kNcclUint64, o, c->comm, c->stream);
+            for (int q = 0; q < world && r == 0; ++q)
+                if (rv[q].n) { r = api->Recv(stage + off, rv[q].n * 4u, kNcclUint64, q, c->comm, c->stream); off += rv[q].n * 4u; }
+        } else {
+            r = api->ReduceScatter(c->bins, c->bins + slice * (size_t)rank, slice, kNcclUint64, kNcclSum, c->comm, c->stream);
+        }
         if (r == 0) r = api->AllReduce(tot, tot, 12, kNcclUint64, kNcclSum, c->comm, c->stream);
         ncclResult_t r2 = api->GroupEnd();
         if (r == 0) r = r2;
         if (r != 0) return fail(c, SINET_E_NCCL, std::string("NCCL reduce: ") + api->GetErrorString(r));
+        if (sparse) {
+            const unsigned long long* stage = reinterpret_cast<const unsigned long long*>(c->d_ws + c->ws.staging);
+            size_t off = 0;
+            for (int q = 0; q < world; ++q)
+                if (rv[q].n) {
+                    SINET_CUDA(c, launch_add_bins(c->bins, stage + off, rv[q].first, rv[q].n, c->sm_count, c->stream));
+                    c->launches++;
+                    off += rv[q].n * 4u;
+                }
+        }
+        c->last_exchange = sparse ? 2 : 1;
     }
     c->reduced = true;
+    return SINET_OK;
+}
+
+int sinet_last_exchange(const sinet_ctx* c) { return c ? c->last_exchange : 0; }
+
+int sinet_touched_range(sinet_ctx* c, uint32_t* min_bin, uint32_t* max_bin) {
+    if (!c || !min_bin || !max_bin) return SINET_E_INVAL;
+    DeviceGuard dg(c->device);
+    uint32_t h[2];
+    SINET_CUDA(c, cudaMemcpyAsync(h, c->d_ws + c->ws.counters + 16, 8, cudaMemcpyDeviceToHost, c->stream));
+    SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    *min_bin = h[0];
+    *max_bin = h[1];
+    return SINET_OK;
+}
+
+int sinet_set_exchange(sinet_ctx* c, int mode) {
+    if (!c || mode < 0 || mode > 2) return c ? fail(c, SINET_E_INVAL, "exchange mode must be 0, 1 or 2") : SINET_E_INVAL;
+    c->exchange = mode;
     return SINET_OK;
 }
 

@@ -145,6 +145,17 @@ __device__ __forceinline__ void flush_totals(const WarpTotals& t, unsigned long 
     }
 }
 
+// Record the extent of the bins this launch wrote (warp-uniform call): the multi-GPU
+// reduce only exchanges the bins inside every rank's touched range.
+__device__ __forceinline__ void note_touched_warp(const KernelParams& p, uint32_t tmin, uint32_t tmax) {
+    tmin = __reduce_min_sync(kFull, tmin);
+    tmax = __reduce_max_sync(kFull, tmax);
+    if ((threadIdx.x & 31u) == 0 && tmin <= tmax) {
+        atomicMin(p.touched, tmin);
+        atomicMax(p.touched + 1, tmax);
+    }
+}
+
 // ---------------------------------------------------------------- a2: columnar record load
 struct Rec4 {
     uint64_t ts[4];

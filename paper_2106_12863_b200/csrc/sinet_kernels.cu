@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
     const uint64_t stride = (uint64_t)gridDim.x * warps_per_block * 128ull;
     WarpTotals tot;
     tot.zero();
+    uint32_t tmin = 0xFFFFFFFFu, tmax = 0u;
 
     for (uint64_t wbase = gw * 128ull; wbase < p.nv; wbase += stride) {
         const uint64_t base = wbase + lane * 4ull;
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
             uint32_t bin = 0;
             const bool inw = map_bin(r.ts[j], p, bin);
             const bool directed = valid && dir < 2u;
+            if (directed && inw) { tmin = min(tmin, bin); tmax = max(tmax, bin); }
             if (directed && inw) {
                 unsigned long long* slot = p.bins + ((size_t)bin * 4u + dir * 2u);
                 atomicAdd(slot, 1ull);
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
         }
         if (p.tags) store_tags4(p, base, tag4);
     }
+    note_touched_warp(p, tmin, tmax);
     flush_totals(tot, p.totals, s_tot);
 }
 

@@ -43,6 +43,7 @@ struct KernelParams {
     uint32_t ranges_per_group;     // 0 = default: record ranges handed out per group (load balance)
     uint32_t n_ranges;             // set by the launcher
     uint32_t* range_counter;       // zeroed by the launcher before each launch
+    uint32_t* touched;             // [2] min / max binned bin of this epoch (sparse multi-GPU exchange)
     const uint32_t* wbits;         // NEXT-2 watchlist: [2048] bitmap of /16 blocks holding a listed address
     const uint32_t* wlist;         // sorted distinct listed addresses
     uint32_t wn;                   // 0 = no watchlist

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
     const uint64_t stride = (uint64_t)gridDim.x * wpb * 128ull;
     WarpTotals tot;
     tot.zero();
+    uint32_t tmin = 0xFFFFFFFFu, tmax = 0u;
     for (uint64_t wbase = gw * 128ull; wbase < p.nv; wbase += stride) {
         const uint64_t base = wbase + lane * 4ull;
         Rec4 r;
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
             uint32_t bin = 0;
             const bool inw = map_bin(r.ts[j], p, bin);
             const bool directed = valid && dir < 2u;
+            if (directed && inw) { tmin = min(tmin, bin); tmax = max(tmax, bin); }
             if (inrange) {   // every record gets a key: filtered or unbinned ones the sentinel
                 const uint64_t a = base + j - p.head;
                 keys[a] = (directed && inw) ? bin * 2u + dir : sentinel;
@@ -56,6 +58,7 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
             tot.add(valid, cell, directed && !inw, dir, r.by[j]);
         }
     }
+    note_touched_warp(p, tmin, tmax);
     flush_totals(tot, p.totals, s_tot);
 }
 

@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     }
     WarpTotals tot;
     tot.zero();
+    uint32_t gmin = 0xFFFFFFFFu, gmax = 0u;   // extent of this group's binned records (uniform)
     for (;;) {
     if (tid == 0) s_range[gid] = atomicAdd(p.range_counter, 1u);
     group_sync();
@@ -415,6 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             }
         }
 
+        if (any) { gmin = min(gmin, bmin); gmax = max(gmax, bmax); }
         if (any) {   // every resident tile this chunk reaches joins the hull
             hull_lo = min(hull_lo, bmin_t > lo_t ? bmin_t : lo_t);
             hull_hi = max(hull_hi, bmax_t);
@@ -485,6 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         claim_and_retire(act_t, lo_t + NT);
     }
     }   // ranges
+    if (tid == 0 && gmin <= gmax) { atomicMin(p.touched, gmin); atomicMax(p.touched + 1, gmax); }
     __syncthreads();
     if (kSmemTot) {
         if (threadIdx.x < 12) {

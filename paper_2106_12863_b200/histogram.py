@@ -187,6 +187,20 @@ class SinetHistogram:
     def reduce(self):
         check(lib.sinet_reduce(self.ctx), self.ctx, "reduce")
 
+    def set_exchange(self, mode: int):
+        """Multi-GPU merge: 0 auto, 1 dense reduce-scatter, 2 sparse touched-range exchange."""
+        check(lib.sinet_set_exchange(self.ctx, mode), self.ctx, "set_exchange")
+
+    def touched_range(self):
+        """(min bin, max bin) written since the last reset; min > max if none."""
+        a, b = ctypes.c_uint32(), ctypes.c_uint32()
+        check(lib.sinet_touched_range(self.ctx, ctypes.byref(a), ctypes.byref(b)), self.ctx, "touched_range")
+        return a.value, b.value
+
+    @property
+    def last_exchange(self) -> int:
+        return int(lib.sinet_last_exchange(self.ctx))
+
     def owned_range(self):
         lo, n = ctypes.c_uint64(), ctypes.c_uint64()
         check(lib.sinet_owned_range(self.ctx, ctypes.byref(lo), ctypes.byref(n)), self.ctx, "owned_range")
@@ -261,6 +275,17 @@ class SinetHistogram:
         ms, k = ctypes.c_double(), ctypes.c_uint64()
         check(lib.sinet_kernel_time(self.ctx, ctypes.byref(ms), ctypes.byref(k)), self.ctx, "kernel_time")
         return ms.value, k.value
+
+
+def exchange_plan(world: int, rank: int, nbins: int, nbins_pad: int, touched):
+    """Host plan of the sparse multi-GPU exchange: (send, recv) int arrays [world, 2] of (first bin, count)."""
+    t = np.ascontiguousarray(np.asarray(touched, dtype=np.uint32).reshape(world * 2))
+    send = np.zeros(world * 2, np.uint64)
+    recv = np.zeros(world * 2, np.uint64)
+    check(lib.sinet_exchange_plan(world, rank, nbins, nbins_pad, t.ctypes.data_as(ctypes.c_void_p),
+                                  send.ctypes.data_as(ctypes.c_void_p), recv.ctypes.data_as(ctypes.c_void_p)),
+          None, "exchange_plan")
+    return send.reshape(world, 2).astype(np.int64), recv.reshape(world, 2).astype(np.int64)
 
 
 def table_member_host(nets, lens, ips) -> np.ndarray:

@@ -359,3 +359,25 @@ def test_watchlist_parity(S, oracle_lib, strategy):
         h.reset()
         h.classify(*d)
         assert int(h.read_totals()[:4].sum()) == wl.n
+
+
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_touched_range_is_binned_extent(S, oracle_lib, strategy):
+    """The extent the sparse multi-GPU exchange relies on: min/max bin with data."""
+    wl = WORKLOADS["c1"].with_(n=200_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    nz = np.nonzero((o.count[0] + o.count[1]) > 0)[0]
+    for sr in (False, True):
+        h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, order=strategy)
+        d = dev_cols(cols)
+        (h.classify_sortreduce if sr else h.classify)(*(c[5000:150_000] for c in d))
+        sub = oracle_lib.classify_histogram(*(c[5000:150_000] for c in cols), nets, lens, wl.window_start_ms,
+                                            wl.window_ms, 1)
+        snz = np.nonzero((sub.count[0] + sub.count[1]) > 0)[0]
+        assert h.touched_range() == (int(snz.min()), int(snz.max()))
+        h.reset()
+        assert h.touched_range() == (0xFFFFFFFF, 0)
+        h.classify(*d)
+        assert h.touched_range() == (int(nz.min()), int(nz.max()))

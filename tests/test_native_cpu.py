@@ -112,3 +112,17 @@ def test_shard_and_owned_ranges_partition():
             own = [owned_bin_range(nbins, r, world) for r in range(world)]
             assert own[0][0] == 0 and own[-1][1] == nbins
             assert all(own[i][1] == own[i + 1][0] for i in range(world - 1))
+
+
+def test_exchange_plan_edges():
+    from paper_2106_12863_b200 import exchange_plan
+    # rank 1 of 4 owns [250, 500) of B = 1000 (pad 1024 -> per 256: [256, 512))
+    t = np.array([[0, 300], [200, 600], [0xFFFFFFFF, 0], [999, 999]], np.uint32)
+    send, recv = exchange_plan(4, 1, 1000, 1024, t)
+    assert send[1].tolist() == [0, 0]                      # nothing to myself
+    assert send[0].tolist() == [200, 56]                   # my [200,600] ∩ own(0)=[0,256)
+    assert send[2].tolist() == [512, 89]                   # ∩ own(2)=[512,768)
+    assert recv[0].tolist() == [256, 45]                   # rank 0's [0,300] ∩ own(1)=[256,512)
+    assert recv[2].tolist() == [0, 0] and recv[3].tolist() == [0, 0]   # empty / disjoint
+    with pytest.raises(N.SinetError):
+        exchange_plan(3, 0, 1000, 1024, t[:3])             # pad not a multiple of world
