@@ -119,15 +119,15 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
     }
 }
 
-// Shared-memory window: a ring of NT tiles x 512 ms bins, 6 u32 per bin =
-// {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in}.  Tiles [lo_t, lo_t + NT)
+// Shared-memory window: a ring of NT tiles x 256 ms bins, stored as six u32 arrays of WS
+// slots (struct of arrays) {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in}.  Tiles [lo_t, lo_t + NT)
 // are resident.  After a chunk is accumulated, tiles below the chunk's
 // oldest bin (keeping >= NT/2-1 tiles of history) are claimed with one
 // non-blocking CAS each; the CAS resolves while the next chunk is loaded and
 // classified, and the tiles are retired (stored or added) right after.  A CTA
 // never waits on another CTA's tile while it holds an unreleased claim, so
 // the protocol cannot deadlock.
-template <int THREADS, int NG, int WS, int RPT, bool kAgg, bool kW1, bool kSmall>
+template <int THREADS, int NG, int WS, int RPT, bool kAgg, bool kW1, bool kSmall, bool kWatch>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // RPT records per thread per chunk; with RPT == 2 the side totals live in shared
     // memory per warp (registers for 1024 threads)
@@ -189,6 +189,28 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             }
         }
     };
+    // write (won: plain stores) or add (RED) 4 consecutive bins of the ring to HBM and zero them
+    auto flush_quad = [&](uint32_t bin0, bool won) {
+        const uint32_t s0 = bin0 & (WS - 1);
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (uint32_t dir = 0; dir < 2; ++dir) {   // one direction at a time: fewer live registers
+            uint4* pc = reinterpret_cast<uint4*>(s_win + dir * WS + s0);
+            uint4* pl = reinterpret_cast<uint4*>(s_win + (2 + dir) * WS + s0);
+            uint4* ph = reinterpret_cast<uint4*>(s_win + (4 + dir) * WS + s0);
+            const uint4 c = *pc, l = *pl, h = *ph;
+            *pc = z; *pl = z; *ph = z;
+            const uint32_t cc[4] = {c.x, c.y, c.z, c.w}, ll[4] = {l.x, l.y, l.z, l.w}, hh[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned long long bb = (unsigned long long)ll[q] | ((unsigned long long)hh[q] << 32);
+                unsigned long long* g64 = p.bins + (size_t)(bin0 + q) * 4u + dir * 2u;
+                if (won) __stcg(reinterpret_cast<ulonglong2*>(g64), make_ulonglong2(cc[q], bb));
+                else if (cc[q]) { atomicAdd(g64, (unsigned long long)cc[q]); if (bb) atomicAdd(g64 + 1, bb); }
+            }
+        }
+    };
+
     // retire tiles [t_from, t_to) whose claims are resolved in s_state (block-uniform call;
     // must be preceded by a barrier after the claims were resolved)
     auto retire = [&](uint32_t t_from, uint32_t t_to) {
@@ -202,34 +224,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t t = t_from + tid, st = s_state[t & (NT - 1)];
             my_o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
         }
-        // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem
+        // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem.
+        // Work items are (tile, 4 consecutive bins): 128-bit shared loads of each field.
         for (uint32_t k = 0; k < nt; ++k) {
-            const uint32_t t = t_from + k, slot = t & (NT - 1);
+            const uint32_t t = t_from + k;
             if (!touched(t)) continue;
-            const uint32_t st = s_state[slot];
+            const uint32_t st = s_state[t & (NT - 1)];
+            if (((st >> 2) != t + 1u) || (st & 3u) == kBusy) busy = true;
+        }
+        for (uint32_t it = tid; it < nt * (kTileBins / 4u); it += GT) {
+            const uint32_t t = t_from + it / (kTileBins / 4u);
+            if (!touched(t)) continue;
+            const uint32_t st = s_state[t & (NT - 1)];
             const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
-            if (o == kBusy) { busy = true; continue; }
-            for (uint32_t i = tid; i < kTileBins; i += GT) {
-                const uint32_t bin = t * kTileBins + i;
-                uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
-                const uint2 c = *reinterpret_cast<const uint2*>(s);
-                const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
-                const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
-                const unsigned long long b_out = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
-                const unsigned long long b_in = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
-                if (o == kWon) {
-                    ulonglong2* g = reinterpret_cast<ulonglong2*>(p.bins + (size_t)bin * 4u);
-                    __stcg(g, make_ulonglong2(c.x, b_out));
-                    __stcg(g + 1, make_ulonglong2(c.y, b_in));
-                } else {
-                    unsigned long long* g64 = p.bins + (size_t)bin * 4u;
-                    if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (b_out) atomicAdd(g64 + 1, b_out); }
-                    if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y); if (b_in) atomicAdd(g64 + 3, b_in); }
-                }
-                *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
-                *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
-                *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
-            }
+            if (o == kBusy) continue;
+            flush_quad(t * kTileBins + (it % (kTileBins / 4u)) * 4u, o == kWon);
         }
         group_sync();
         // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones
@@ -252,28 +261,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         }
         if (busy) {
             group_sync();
-            for (uint32_t k = 0; k < nt; ++k) {
-                const uint32_t t = t_from + k, slot = t & (NT - 1);
+            for (uint32_t it = tid; it < nt * (kTileBins / 4u); it += GT) {
+                const uint32_t t = t_from + it / (kTileBins / 4u);
                 if (!touched(t)) continue;
-                const uint32_t st = s_state[slot];
+                const uint32_t st = s_state[t & (NT - 1)];
                 if (((st >> 2) == t + 1u) && (st & 3u) != kBusy) continue;
-                for (uint32_t i = tid; i < kTileBins; i += GT) {
-                    const uint32_t bin = t * kTileBins + i;
-                    uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
-                    const uint2 c = *reinterpret_cast<const uint2*>(s);
-                    const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
-                    const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
-                    unsigned long long* g64 = p.bins + (size_t)bin * 4u;
-                    if (c.x) { atomicAdd(g64, (unsigned long long)c.x);
-                               const unsigned long long v = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
-                               if (v) atomicAdd(g64 + 1, v); }
-                    if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y);
-                               const unsigned long long v = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
-                               if (v) atomicAdd(g64 + 3, v); }
-                    *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
-                    *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
-                    *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
-                }
+                flush_quad(t * kTileBins + (it % (kTileBins / 4u)) * 4u, false);
             }
             group_sync();
         }
@@ -291,13 +284,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 
     // accumulate (cnt, bytes) of one (bin, dir) into the ring (caller checked residency)
     auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) {
-        uint32_t* s = s_win + (bin & (WS - 1)) * 6u + dir;
+        uint32_t* s = s_win + dir * WS + (bin & (WS - 1));
         atomicAdd(s, cnt);
         const uint32_t lo = (uint32_t)bytes;
         uint32_t hi = (uint32_t)(bytes >> 32);
-        const uint32_t old = atomicAdd(s + 2, lo);
+        const uint32_t old = atomicAdd(s + 2 * WS, lo);
         hi += (old + lo < old) ? 1u : 0u;     // exact carry out of the low word
-        if (hi) atomicAdd(s + 4, hi);
+        if (hi) atomicAdd(s + 4 * WS, hi);
     };
 
     // Contiguous ranges of 4-record groups (virtual index space) are handed out
@@ -347,7 +340,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         WarpTotals& tt = kSmemTot ? ctot : tot;
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const bool valid = (full || (have && vvalid(p, my_v + j))) && watch_pass(cur.src[j], cur.dst[j], p);
+            const bool valid = (full || (have && vvalid(p, my_v + j))) &&
+                               (!kWatch || watched(cur.src[j], p) || watched(cur.dst[j], p));
             const uint32_t s_in = member(cur.src[j], T);
             const uint32_t d_in = member(cur.dst[j], T);
             const uint32_t cell = s_in * 2u + d_in;
@@ -424,6 +418,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         const bool key32 = p.nbins < 0x40000000u;   // keys 2*bin+dir stay below the lane sentinels
 
         // ---- a6 (accumulate): reduce the chunk into the ring
+        // the whole chunk inside the ring (the common case): no per-record residency/spill checks
+        const bool all_in = any && bmin_t >= lo_t && bmax_t - lo_t < NT;
+        if (!kAgg && all_in) {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j)
+                if (binned4[j]) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
+        } else
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const bool b = binned4[j];
@@ -509,19 +510,20 @@ constexpr int kRingBins1 = 8192;
 constexpr int kRingBins2 = 4096;
 }  // namespace
 
-// (threads, groups, records per thread): 512/1/4, 512/2/4, 1024/1/2, 1024/2/2
-#define SINET_STREAM_KERNEL(TH, G, A, W, S) \
-    k_hist_stream<TH, G, (G == 1 ? kRingBins1 : kRingBins2), (TH == 512 ? 4 : 2), A, W, S>
+// 512 threads x 4 records per thread; one group (8192-bin ring) or two (4096-bin rings).
+// (The kernel also supports 1024 threads x 2 records, measured 23 % slower: not instantiated.)
+#define SINET_STREAM_KERNEL(G, A, W, S, WL) \
+    k_hist_stream<512, G, (G == 1 ? kRingBins1 : kRingBins2), 4, A, W, S, WL>
 
 cudaError_t setup_hist_stream() {
     const int mx = (int)((size_t)kRingBins1 * 6u * 4u + kMaxTableSmem);
     cudaError_t e;
-#define SET(TH, G, A, W, S)                                                                                 \
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(TH, G, A, W, S), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
+#define SET(G, A, W, S, WL)                                                                                 \
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W, S, WL), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
-#define SET4(TH, G, S) SET(TH, G, true, true, S) SET(TH, G, true, false, S) SET(TH, G, false, true, S) SET(TH, G, false, false, S)
-    SET4(512, 1, true) SET4(512, 1, false) SET4(512, 2, true) SET4(512, 2, false)
-    SET4(1024, 1, true) SET4(1024, 1, false) SET4(1024, 2, true) SET4(1024, 2, false)
+#define SET4(G, S, WL) SET(G, true, true, S, WL) SET(G, true, false, S, WL) SET(G, false, true, S, WL) SET(G, false, false, S, WL)
+    SET4(1, true, false) SET4(1, false, false) SET4(2, true, false) SET4(2, false, false)
+    SET4(1, true, true) SET4(1, false, true) SET4(2, true, true) SET4(2, false, true)
 #undef SET4
 #undef SET
     return cudaSuccess;
@@ -536,7 +538,6 @@ int stream_groups_for(const KernelParams& p) {
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st) {
     static_assert(kRingBins1 == 2 * kRingBins2, "both layouts use the same shared memory");
     const size_t sm = (size_t)kRingBins1 * 6u * 4u + table_smem_bytes(p.nbnd, p.n_mixed, p.small);
-    const int th = (p.stream_threads == 1024) ? 1024 : 512;
     const uint64_t chunks = (p.nv / 4 + 511) / 512;
     const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
     const bool w1 = p.width == 1u;
@@ -547,14 +548,14 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
     cudaError_t e = cudaMemsetAsync(p.range_counter, 0, 8, st);
     if (e != cudaSuccess) return e;
-#define LAUNCH(TH, G, S)                                                                                \
-    if (agg && w1) SINET_STREAM_KERNEL(TH, G, true, true, S)<<<grid, TH, sm, st>>>(q);                  \
-    else if (agg) SINET_STREAM_KERNEL(TH, G, true, false, S)<<<grid, TH, sm, st>>>(q);                  \
-    else if (w1) SINET_STREAM_KERNEL(TH, G, false, true, S)<<<grid, TH, sm, st>>>(q);                   \
-    else SINET_STREAM_KERNEL(TH, G, false, false, S)<<<grid, TH, sm, st>>>(q);
-#define LAUNCH_G(TH, S) if (g == 2) { LAUNCH(TH, 2, S) } else { LAUNCH(TH, 1, S) }
-    if (th == 1024) { if (p.small) { LAUNCH_G(1024, true) } else { LAUNCH_G(1024, false) } }
-    else { if (p.small) { LAUNCH_G(512, true) } else { LAUNCH_G(512, false) } }
+#define LAUNCH(G, S, WL)                                                                                \
+    if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S, WL)<<<grid, 512, sm, st>>>(q);                  \
+    else if (agg) SINET_STREAM_KERNEL(G, true, false, S, WL)<<<grid, 512, sm, st>>>(q);                  \
+    else if (w1) SINET_STREAM_KERNEL(G, false, true, S, WL)<<<grid, 512, sm, st>>>(q);                   \
+    else SINET_STREAM_KERNEL(G, false, false, S, WL)<<<grid, 512, sm, st>>>(q);
+#define LAUNCH_G(S, WL) if (g == 2) { LAUNCH(2, S, WL) } else { LAUNCH(1, S, WL) }
+    if (p.wn) { if (p.small) { LAUNCH_G(true, true) } else { LAUNCH_G(false, true) } }
+    else { if (p.small) { LAUNCH_G(true, false) } else { LAUNCH_G(false, false) } }
 #undef LAUNCH_G
 #undef LAUNCH
     return cudaGetLastError();
