@@ -119,8 +119,9 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
     }
 }
 
-// Shared-memory window: a ring of NT tiles x 256 ms bins, stored as six u32 arrays of WS
-// slots (struct of arrays) {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in}.  Tiles [lo_t, lo_t + NT)
+// Shared-memory window: a ring of NT tiles x 256 ms bins, 6 u32 per bin =
+// {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in} (array of structs: a thread retires one
+// bin as one full 32-byte sector, so a warp writes 1 KB contiguous per store pair).  Tiles [lo_t, lo_t + NT)
 // are resident.  After a chunk is accumulated, tiles below the chunk's
 // oldest bin (keeping >= NT/2-1 tiles of history) are claimed with one
 // non-blocking CAS each; the CAS resolves while the next chunk is loaded and
@@ -190,24 +191,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         }
     };
     // write (won: plain stores) or add (RED) 4 consecutive bins of the ring to HBM and zero them
-    auto flush_quad = [&](uint32_t bin0, bool won) {
-        const uint32_t s0 = bin0 & (WS - 1);
-        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-        for (uint32_t dir = 0; dir < 2; ++dir) {   // one direction at a time: fewer live registers
-            uint4* pc = reinterpret_cast<uint4*>(s_win + dir * WS + s0);
-            uint4* pl = reinterpret_cast<uint4*>(s_win + (2 + dir) * WS + s0);
-            uint4* ph = reinterpret_cast<uint4*>(s_win + (4 + dir) * WS + s0);
-            const uint4 c = *pc, l = *pl, h = *ph;
-            *pc = z; *pl = z; *ph = z;
-            const uint32_t cc[4] = {c.x, c.y, c.z, c.w}, ll[4] = {l.x, l.y, l.z, l.w}, hh[4] = {h.x, h.y, h.z, h.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const unsigned long long bb = (unsigned long long)ll[q] | ((unsigned long long)hh[q] << 32);
-                unsigned long long* g64 = p.bins + (size_t)(bin0 + q) * 4u + dir * 2u;
-                if (won) __stcg(reinterpret_cast<ulonglong2*>(g64), make_ulonglong2(cc[q], bb));
-                else if (cc[q]) { atomicAdd(g64, (unsigned long long)cc[q]); if (bb) atomicAdd(g64 + 1, bb); }
-            }
+    // write (won: plain stores) or add (RED) one bin of the ring to HBM and zero it
+    auto flush_bin = [&](uint32_t bin, bool won) {
+        uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
+        const uint2 c = *reinterpret_cast<const uint2*>(s);
+        const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
+        const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
+        *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
+        *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
+        *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
+        const unsigned long long b_out = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
+        const unsigned long long b_in = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
+        unsigned long long* g64 = p.bins + (size_t)bin * 4u;
+        if (won) {
+            ulonglong2* g = reinterpret_cast<ulonglong2*>(g64);
+            __stcg(g, make_ulonglong2(c.x, b_out));
+            __stcg(g + 1, make_ulonglong2(c.y, b_in));
+        } else {
+            if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (b_out) atomicAdd(g64 + 1, b_out); }
+            if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y); if (b_in) atomicAdd(g64 + 3, b_in); }
         }
     };
 
@@ -224,21 +226,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t t = t_from + tid, st = s_state[t & (NT - 1)];
             my_o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
         }
-        // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem.
-        // Work items are (tile, 4 consecutive bins): 128-bit shared loads of each field.
+        // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem
         for (uint32_t k = 0; k < nt; ++k) {
             const uint32_t t = t_from + k;
             if (!touched(t)) continue;
             const uint32_t st = s_state[t & (NT - 1)];
             if (((st >> 2) != t + 1u) || (st & 3u) == kBusy) busy = true;
         }
-        for (uint32_t it = tid; it < nt * (kTileBins / 4u); it += GT) {
-            const uint32_t t = t_from + it / (kTileBins / 4u);
+        for (uint32_t k = 0; k < nt; ++k) {
+            const uint32_t t = t_from + k;
             if (!touched(t)) continue;
             const uint32_t st = s_state[t & (NT - 1)];
             const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
             if (o == kBusy) continue;
-            flush_quad(t * kTileBins + (it % (kTileBins / 4u)) * 4u, o == kWon);
+            for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin(t * kTileBins + i, o == kWon);
         }
         group_sync();
         // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones
@@ -261,12 +262,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         }
         if (busy) {
             group_sync();
-            for (uint32_t it = tid; it < nt * (kTileBins / 4u); it += GT) {
-                const uint32_t t = t_from + it / (kTileBins / 4u);
+            for (uint32_t k = 0; k < nt; ++k) {
+                const uint32_t t = t_from + k;
                 if (!touched(t)) continue;
                 const uint32_t st = s_state[t & (NT - 1)];
                 if (((st >> 2) == t + 1u) && (st & 3u) != kBusy) continue;
-                flush_quad(t * kTileBins + (it % (kTileBins / 4u)) * 4u, false);
+                for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin(t * kTileBins + i, false);
             }
             group_sync();
         }
@@ -284,13 +285,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 
     // accumulate (cnt, bytes) of one (bin, dir) into the ring (caller checked residency)
     auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) {
-        uint32_t* s = s_win + dir * WS + (bin & (WS - 1));
+        uint32_t* s = s_win + (bin & (WS - 1)) * 6u + dir;
         atomicAdd(s, cnt);
         const uint32_t lo = (uint32_t)bytes;
         uint32_t hi = (uint32_t)(bytes >> 32);
-        const uint32_t old = atomicAdd(s + 2 * WS, lo);
+        const uint32_t old = atomicAdd(s + 2, lo);
         hi += (old + lo < old) ? 1u : 0u;     // exact carry out of the low word
-        if (hi) atomicAdd(s + 4 * WS, hi);
+        if (hi) atomicAdd(s + 4, hi);
     };
 
     // Contiguous ranges of 4-record groups (virtual index space) are handed out

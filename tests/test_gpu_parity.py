@@ -381,3 +381,60 @@ def test_touched_range_is_binned_extent(S, oracle_lib, strategy):
         assert h.touched_range() == (0xFFFFFFFF, 0)
         h.classify(*d)
         assert h.touched_range() == (int(nz.min()), int(nz.max()))
+
+
+# ----------------------------------------------------------------------------- full-size configs
+def _full_records(wl, device="cuda", chunk=200_000_000):
+    """All records of a BASELINE config on the device, generated in chunks (bounded temporaries)."""
+    from synth.sinet_synth import stream_order
+    order = stream_order(wl, device)
+    out = {"ts": torch.empty(wl.n, dtype=torch.int64, device=device),
+           "src": torch.empty(wl.n, dtype=torch.int32, device=device),
+           "dst": torch.empty(wl.n, dtype=torch.int32, device=device),
+           "bytes": torch.empty(wl.n, dtype=torch.int64, device=device)}
+    for lo in range(0, wl.n, chunk):
+        hi = min(wl.n, lo + chunk)
+        r = records(wl, lo, hi, device=device, order=order)
+        for k in out:
+            out[k][lo:hi] = r[k]
+        del r
+    del order
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_full_size_sampled_parity(S, oracle_lib, name):
+    """BASELINE configs[2..4] at full size on one GPU (1.2 B / 1.6 B bursty / 400 M with 4096
+    prefixes), default strategy: full-size properties (conservation, Σbins = totals) plus every
+    sampled bin (random, first/last, the hottest) bit-exact against the oracle run on exactly the
+    records that fall into those bins."""
+    wl = WORKLOADS[name]
+    nets, lens = prefix_table(wl)
+    rec = _full_records(wl)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms)
+    h.classify(rec["ts"], rec["src"], rec["dst"], rec["bytes"])
+    h.finalize()
+    tot = h.read_totals().astype(object)
+    M = (1 << 64) - 1
+    assert int(sum(tot[0:4])) == wl.n
+    assert int(sum(tot[4:8])) & M == int(rec["bytes"].sum().item()) & M
+    bv = h.bins_view()[: wl.nbins]
+    for d, cells in ((0, (2, 3)), (1, (1,))):   # SRC_PRIORITY: OUT = cells 2,3; IN = cell 1
+        csum = int(bv[:, d, 0].sum().item()) & M
+        bsum = int(bv[:, d, 1].sum().item()) & M
+        assert (csum + int(tot[8 + d])) & M == sum(int(tot[k]) for k in cells) & M
+        assert (bsum + int(tot[10 + d])) & M == sum(int(tot[4 + k]) for k in cells) & M
+    g = torch.Generator(device="cpu").manual_seed(2106)
+    hot = int(torch.argmax(bv[:, 0, 0] + bv[:, 1, 0]).item())
+    pick = torch.cat([torch.randint(0, wl.nbins, (384,), generator=g),
+                      torch.tensor([0, 1, wl.nbins - 2, wl.nbins - 1, hot])]).to("cuda")
+    sel = torch.isin((rec["ts"] - wl.window_start_ms) // wl.bin_width_ms, pick)
+    cols = (rec["ts"][sel].cpu().numpy().view(np.uint64), rec["src"][sel].cpu().numpy().view(np.uint32),
+            rec["dst"][sel].cpu().numpy().view(np.uint32), rec["bytes"][sel].cpu().numpy().view(np.uint64))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, wl.bin_width_ms)
+    p = pick.cpu().numpy()
+    got = bv[pick].cpu().numpy().view(np.uint64)
+    np.testing.assert_array_equal(got[:, :, 0].T, o.count[:, p])
+    np.testing.assert_array_equal(got[:, :, 1].T, o.bytes[:, p])
