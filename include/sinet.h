@@ -130,10 +130,21 @@ size_t sinet_staging_bytes(uint64_t chunk_records);
  * Errors: E_INVAL (n_prefixes == 0, a prefix_len > 32, bin_width 0, W % w != 0,
  * W == 0 or W >= 2^32, window_start + W overflows, world < 1, rank outside
  * [0,world), dir_lut entry > 2, reserved != 0, buffer too small or misaligned),
- * E_CUDA. */
+ * E_CUDA.  At most 16383 entries. */
 int sinet_open(sinet_ctx** out, const sinet_config* cfg,
                const uint32_t* prefix_net, const uint8_t* prefix_len, uint32_t n_prefixes,
                void* d_bins, size_t bins_bytes, void* d_ws, size_t ws_bytes);
+
+/* NEXT-4, labelled longest-prefix match: as sinet_open, but entry i carries
+ * prefix_label[i] (1 = SINET inside, 0 = carved out) and an address is inside iff
+ * the longest entry matching it (Alg. 1 l.6-9 per entry) is labelled inside;
+ * unmatched addresses are outside; of equal (Y/Z) entries the last one wins.
+ * prefix_label == NULL is sinet_open (every entry inside: match-any).  The
+ * labelled table is compiled to the same member intervals, so every kernel is
+ * unchanged.  At most 16383 entries.  Errors: as sinet_open. */
+int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg,
+                        const uint32_t* prefix_net, const uint8_t* prefix_len, const uint8_t* prefix_label,
+                        uint32_t n_prefixes, void* d_bins, size_t bins_bytes, void* d_ws, size_t ws_bytes);
 
 /* Destroy a ctx (does not free caller memory).  NULL is a no-op. */
 void sinet_close(sinet_ctx* ctx);
@@ -272,6 +283,10 @@ int sinet_last_strategy(const sinet_ctx* ctx);
  * Errors: E_INVAL as sinet_open's table checks. */
 int sinet_table_member_host(const uint32_t* prefix_net, const uint8_t* prefix_len, uint32_t n_prefixes,
                             const uint32_t* ips, uint64_t n, uint8_t* out);
+/* The same for a labelled table (sinet_open_labelled semantics). */
+int sinet_table_member_host_labelled(const uint32_t* prefix_net, const uint8_t* prefix_len,
+                                     const uint8_t* prefix_label, uint32_t n_prefixes,
+                                     const uint32_t* ips, uint64_t n, uint8_t* out);
 /* Performance knobs of the STREAM kernel (results are identical for every setting):
  * stream_groups 0 = automatic, 1 = one 8192-bin ring per CTA, 2 = two independent
  * 4096-bin rings per CTA; warp_aggregation 1/0 = on/off, -1 = unchanged.  Errors: E_INVAL. */

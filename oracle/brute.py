@@ -63,3 +63,14 @@ def histogram_counter(ts, src, dst, nbytes, nets, lens, start, window, width, lu
     byt = Counter({k: v & M64 for k, v in byt.items()})
     return (cnt, byt, [c & M64 for c in m_count], [c & M64 for c in m_bytes],
             [c & M64 for c in oow_c], [c & M64 for c in oow_b])
+
+
+def member_lpm_bitstring(ip: int, nets, lens, labels) -> bool:
+    """Longest matching prefix (by bit strings) decides; no match -> outside."""
+    s = bits32(ip)
+    best, lab = -1, False
+    for n, z, l in zip(nets, lens, labels):
+        z = int(z)
+        if s[:z] == bits32(int(n))[:z] and z >= best:
+            best, lab = z, bool(l)
+    return lab

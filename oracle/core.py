@@ -58,6 +58,11 @@ def _load():
         lib.oracle_tags.argtypes = [u64p, u32p, u32p, ctypes.c_uint64, u32p, u8p, ctypes.c_uint32,
                                     ctypes.c_uint64, ctypes.c_uint64, u8p]
         lib.oracle_tags.restype = None
+        lib.oracle_histogram_members.argtypes = [u64p, u8p, u8p, u64p, ctypes.c_uint64, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.c_uint32, u8p, u64p, u64p, u64p]
+        lib.oracle_histogram_members.restype = None
+        lib.oracle_member_lpm_batch.argtypes = [u32p, ctypes.c_uint64, u32p, u8p, u8p, ctypes.c_uint32, u8p]
+        lib.oracle_member_lpm_batch.restype = None
         lib.oracle_watch_filter.argtypes = [u32p, u32p, ctypes.c_uint64, u32p, ctypes.c_uint32, u64p]
         lib.oracle_watch_filter.restype = ctypes.c_uint64
         lib.oracle_rebin.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, u64p]
@@ -201,3 +206,31 @@ def classify_histogram_watched(ts, src, dst, nbytes, nets, lens, watchlist, star
     keep = watch_filter(src, dst, watchlist)
     cols = [np.ascontiguousarray(np.asarray(c)[keep]) for c in (ts, src, dst, nbytes)]
     return classify_histogram(*cols, nets, lens, start, window, width, lut=lut, threads=threads)
+
+
+def member_lpm(ips, nets, lens, labels) -> np.ndarray:
+    """NEXT-4: membership under a labelled table (longest matching prefix decides)."""
+    ips = np.ascontiguousarray(np.asarray(ips, dtype=np.uint32))
+    nets, lens = _table(nets, lens)
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.uint8))
+    out = np.zeros(len(ips), np.uint8)
+    _load().oracle_member_lpm_batch(_ptr(ips, ctypes.c_uint32), len(ips), _ptr(nets, ctypes.c_uint32),
+                                    _ptr(lens, ctypes.c_uint8), _ptr(lab, ctypes.c_uint8), len(nets),
+                                    _ptr(out, ctypes.c_uint8))
+    return out
+
+
+def classify_histogram_lpm(ts, src, dst, nbytes, nets, lens, labels, start, window, width,
+                           lut=LUT_SRC_PRIORITY) -> OracleResult:
+    """NEXT-4: the histogram with membership decided by the labelled longest-prefix match."""
+    ts = np.ascontiguousarray(ts, dtype=np.uint64)
+    nbytes = np.ascontiguousarray(nbytes, dtype=np.uint64)
+    s_in = member_lpm(src, nets, lens, labels)
+    d_in = member_lpm(dst, nets, lens, labels)
+    res = OracleResult(window // width)
+    lut_a = np.ascontiguousarray(np.asarray(lut, dtype=np.uint8))
+    _load().oracle_histogram_members(_ptr(ts, ctypes.c_uint64), _ptr(s_in, ctypes.c_uint8), _ptr(d_in, ctypes.c_uint8),
+                                     _ptr(nbytes, ctypes.c_uint64), len(ts), start, window, width,
+                                     _ptr(lut_a, ctypes.c_uint8), _ptr(res.count, ctypes.c_uint64),
+                                     _ptr(res.bytes, ctypes.c_uint64), _ptr(res.totals, ctypes.c_uint64))
+    return res

@@ -262,3 +262,61 @@ uint64_t oracle_watch_filter(const uint32_t* src, const uint32_t* dst, uint64_t 
             keep[k++] = r;
     return k;
 }
+
+/* ---------------------------------------------------------------------- */
+/* NEXT-4, labelled longest-prefix match.  A table entry Y/Z carries a label
+ * (1 = SINET inside, 0 = carved out); an address is inside iff the longest
+ * entry whose Alg. 1 test matches it (l.6-9) is labelled inside,
+ * outside if no entry matches (reading A26 in DESIGN.md).  With every label 1
+ * this is oracle_member().  Equal (net, Z) entries: the last one wins.
+ * Linear scan, literal mask-and-subtract.                                   */
+int oracle_member_lpm(uint32_t ip, const uint32_t* nets, const uint8_t* lens, const uint8_t* labels,
+                      uint32_t p)
+{
+    int best_len = -1, best_label = 0;
+    for (uint32_t i = 0; i < p; ++i) {
+        uint32_t z = lens[i];
+        uint32_t sb = oracle_bitmask(ip, z);
+        uint32_t cb = oracle_bitmask(nets[i], z);
+        if (sb - cb == 0u && (int)z >= best_len) {
+            best_len = (int)z;
+            best_label = labels[i] ? 1 : 0;
+        }
+    }
+    return best_label;
+}
+
+/* Per-address membership under a labelled table (for the histogram oracle the
+ * labelled table is applied through oracle_lpm_to_members(): it lists the
+ * member addresses' membership bits for a batch). */
+void oracle_member_lpm_batch(const uint32_t* ips, uint64_t n, const uint32_t* nets, const uint8_t* lens,
+                             const uint8_t* labels, uint32_t p, uint8_t* out)
+{
+    for (uint64_t r = 0; r < n; ++r) out[r] = (uint8_t)oracle_member_lpm(ips[r], nets, lens, labels, p);
+}
+
+/* The histogram of oracle_classify_histogram with the memberships given per
+ * record (s_in[r], d_in[r] in {0,1}), e.g. from oracle_member_lpm(): the same
+ * steps after discrimination (LUT, window test, Map, Reduce).               */
+void oracle_histogram_members(const uint64_t* ts, const uint8_t* s_in, const uint8_t* d_in,
+                              const uint64_t* bytes, uint64_t n, uint64_t start, uint64_t window,
+                              uint32_t width, const uint8_t lut[4],
+                              uint64_t* out_count, uint64_t* out_bytes, uint64_t* totals)
+{
+    uint64_t nbins = window / width;
+    for (uint64_t r = 0; r < n; ++r) {
+        int cell = (s_in[r] ? 2 : 0) + (d_in[r] ? 1 : 0);
+        totals[0 + cell] += 1u;
+        totals[4 + cell] += bytes[r];
+        int dir = lut[cell];
+        if (dir != 0 && dir != 1) continue;
+        if (ts[r] < start || ts[r] - start >= window) {
+            totals[8 + dir] += 1u;
+            totals[10 + dir] += bytes[r];
+            continue;
+        }
+        uint64_t key = (ts[r] - start) / (uint64_t)width;
+        out_count[(uint64_t)dir * nbins + key] += 1u;
+        out_bytes[(uint64_t)dir * nbins + key] += bytes[r];
+    }
+}

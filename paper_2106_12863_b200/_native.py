@@ -56,6 +56,7 @@ _SIGS = {
     "sinet_workspace_bytes": ([_CP, _u32], ctypes.c_size_t),
     "sinet_staging_bytes": ([_u64], ctypes.c_size_t),
     "sinet_open": ([ctypes.POINTER(_vp), _CP, _vp, _vp, _u32, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t], _i),
+    "sinet_open_labelled": ([ctypes.POINTER(_vp), _CP, _vp, _vp, _vp, _u32, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t], _i),
     "sinet_close": ([_vp], None),
     "sinet_reset": ([_vp], _i),
     "sinet_classify_histogram": ([_vp, ctypes.POINTER(Records), _vp], _i),
@@ -84,6 +85,7 @@ _SIGS = {
     "sinet_touched_range": ([_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u32)], _i),
     "sinet_exchange_plan": ([ctypes.c_int32, ctypes.c_int32, _u64, _u64, _vp, _vp, _vp], _i),
     "sinet_table_member_host": ([_vp, _vp, _u32, _vp, _u64, _vp], _i),
+    "sinet_table_member_host_labelled": ([_vp, _vp, _vp, _u32, _vp, _u64, _vp], _i),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(lib, _name)

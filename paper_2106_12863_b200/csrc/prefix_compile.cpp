@@ -17,14 +17,64 @@
 
 namespace sinet {
 
+// NEXT-4, labelled longest-prefix match: member intervals of "the longest entry
+// containing ip is labelled inside".  Prefix intervals are laminar (nested or
+// disjoint), so a sweep with a stack of open intervals yields, between
+// consecutive interval edges, the innermost (longest) enclosing entry.
+static void lpm_member_intervals(std::vector<std::pair<uint64_t, uint64_t>>& iv_lo_hi,
+                                 const std::vector<uint8_t>& lab_by_iv,
+                                 std::vector<std::pair<uint64_t, uint64_t>>* members) {
+    // order: start ascending, then wider (outer) first
+    std::vector<size_t> order(iv_lo_hi.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        if (iv_lo_hi[a].first != iv_lo_hi[b].first) return iv_lo_hi[a].first < iv_lo_hi[b].first;
+        return iv_lo_hi[a].second > iv_lo_hi[b].second;
+    });
+    std::vector<size_t> stack;
+    uint64_t cur = 0;   // next address not yet emitted
+    auto emit = [&](uint64_t lo, uint64_t hi_excl, bool in) {
+        if (!in || lo >= hi_excl) return;
+        if (!members->empty() && members->back().second + 1 == lo) members->back().second = hi_excl - 1;
+        else members->emplace_back(lo, hi_excl - 1);
+    };
+    auto top_in = [&]() { return !stack.empty() && lab_by_iv[stack.back()] != 0; };
+    for (size_t k : order) {
+        const uint64_t lo = iv_lo_hi[k].first, hi = iv_lo_hi[k].second;
+        // close every open interval that ends before this one starts
+        while (!stack.empty() && iv_lo_hi[stack.back()].second < lo) {
+            const uint64_t end = iv_lo_hi[stack.back()].second + 1;
+            emit(cur, end, top_in());
+            cur = end;
+            stack.pop_back();
+        }
+        emit(cur, lo, top_in());
+        cur = lo;
+        stack.push_back(k);
+        (void)hi;
+    }
+    while (!stack.empty()) {
+        const uint64_t end = iv_lo_hi[stack.back()].second + 1;
+        emit(cur, end, top_in());
+        cur = end;
+        stack.pop_back();
+    }
+}
+
 bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
                       CompiledTable* out, std::string* err) {
+    return compile_prefixes_labelled(net, len, nullptr, n, out, err);
+}
+
+bool compile_prefixes_labelled(const uint32_t* net, const uint8_t* len, const uint8_t* label, uint32_t n,
+                               CompiledTable* out, std::string* err) {
     if (n == 0) { *err = "empty CIDR list (n_prefixes == 0)"; return false; }
-    if (n > kMaxPrefixes) { *err = "too many prefixes (max 32767)"; return false; }
+    if (n > kMaxPrefixes) { *err = "too many prefixes (max 16383)"; return false; }
     if (!net || !len) { *err = "NULL prefix array"; return false; }
 
     // normalise (Alg. 1 l.7: CB = bitmask(Y, Z)) and form [lo, hi] as u64
     std::vector<std::pair<uint64_t, uint64_t>> iv;
+    std::vector<uint8_t> lab;
     iv.reserve(n);
     for (uint32_t i = 0; i < n; ++i) {
         if (len[i] > 32) {
@@ -36,18 +86,34 @@ bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
         uint64_t host = (len[i] == 0) ? 0xFFFFFFFFull : ((1ull << (32 - len[i])) - 1ull);
         uint64_t lo = (uint64_t)net[i] & ~host & 0xFFFFFFFFull;
         iv.emplace_back(lo, lo | host);
+        lab.push_back(label ? (label[i] ? 1 : 0) : 1);
     }
-    std::sort(iv.begin(), iv.end());
-    iv.erase(std::unique(iv.begin(), iv.end()), iv.end());
-    out->n_unique = (uint32_t)iv.size();
-
-    // merge overlapping or adjacent intervals
     std::vector<std::pair<uint64_t, uint64_t>> merged;
-    for (auto& p : iv) {
-        if (!merged.empty() && p.first <= merged.back().second + 1)
-            merged.back().second = std::max(merged.back().second, p.second);
-        else
-            merged.push_back(p);
+    if (!label) {
+        // plain list: match-any = union of the intervals (reading A3)
+        std::sort(iv.begin(), iv.end());
+        iv.erase(std::unique(iv.begin(), iv.end()), iv.end());
+        out->n_unique = (uint32_t)iv.size();
+        for (auto& p : iv) {
+            if (!merged.empty() && p.first <= merged.back().second + 1)
+                merged.back().second = std::max(merged.back().second, p.second);
+            else
+                merged.push_back(p);
+        }
+    } else {
+        // labelled: equal entries -> the last one wins, then the LPM sweep
+        std::vector<size_t> idx;
+        for (size_t i = 0; i < iv.size(); ++i) idx.push_back(i);
+        std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return iv[a] < iv[b]; });
+        std::vector<std::pair<uint64_t, uint64_t>> uiv;
+        std::vector<uint8_t> ulab;
+        for (size_t k = 0; k < idx.size(); ++k) {
+            if (k + 1 < idx.size() && iv[idx[k + 1]] == iv[idx[k]]) continue;   // a later equal entry wins
+            uiv.push_back(iv[idx[k]]);
+            ulab.push_back(lab[idx[k]]);
+        }
+        out->n_unique = (uint32_t)uiv.size();
+        lpm_member_intervals(uiv, ulab, &merged);
     }
     out->n_intervals = (uint32_t)merged.size();
 
@@ -56,6 +122,7 @@ bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
         out->bnd.push_back((uint32_t)p.first);
         if (p.second < 0xFFFFFFFFull) out->bnd.push_back((uint32_t)(p.second + 1));
     }
+    if (out->bnd.size() > 65535u) { *err = "compiled table too large (> 65535 boundaries)"; return false; }
     const std::vector<uint32_t>& b = out->bnd;
 
     out->cls2.assign(4096, 0u);

@@ -33,10 +33,15 @@ struct CompiledTable {
     uint32_t n_mixed = 0;      // /16 blocks of class 2
 };
 
-constexpr uint32_t kMaxPrefixes = 32767;   // keeps lo and len in 16 bits each
+constexpr uint32_t kMaxPrefixes = 16383;   // <= 4P+2 boundaries keeps lo and len in 16 bits each
 
 // Returns false (with *err set) on invalid input (n == 0, len > 32, n > kMaxPrefixes).
 bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,
                       CompiledTable* out, std::string* err);
+
+// NEXT-4: labelled table (label[i] = 1 inside, 0 carved out); an address is a member iff
+// its longest matching entry is labelled inside.  label == nullptr: every entry inside.
+bool compile_prefixes_labelled(const uint32_t* net, const uint8_t* len, const uint8_t* label, uint32_t n,
+                               CompiledTable* out, std::string* err);
 
 }  // namespace sinet

@@ -115,10 +115,10 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes, int world) {
     L.totals = off; off = align_up(off + 16 * 8, 256);
     L.cls2 = off;   off = align_up(off + (size_t)kClsWords * 4, 256);
     L.entry = off;  off = align_up(off + 65536 * 4, 256);
-    L.bnd = off;    off = align_up(off + ((size_t)2 * n_prefixes + 1) * 4, 256);
+    L.bnd = off;    off = align_up(off + ((size_t)4 * n_prefixes + 2) * 4, 256);
     L.rank = off;   off = align_up(off + (size_t)kRankWords * 4, 256);
-    L.mentry = off; off = align_up(off + (size_t)(2u * n_prefixes + 1u) * 4, 256);
-    L.l2 = off;     off = align_up(off + (size_t)(2u * n_prefixes + 1u) * 64, 256);
+    L.mentry = off; off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 4, 256);
+    L.l2 = off;     off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 64, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
     L.counters = off; off = align_up(off + 64, 256);   // [0] range counter, [4..5] touched min/max
@@ -404,6 +404,12 @@ size_t sinet_staging_bytes(uint64_t chunk_records) {
 int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_net,
                const uint8_t* prefix_len, uint32_t n_prefixes, void* d_bins, size_t bins_bytes,
                void* d_ws, size_t ws_bytes) {
+    return sinet_open_labelled(out, cfg, prefix_net, prefix_len, nullptr, n_prefixes, d_bins, bins_bytes, d_ws, ws_bytes);
+}
+
+int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_net,
+                        const uint8_t* prefix_len, const uint8_t* prefix_label, uint32_t n_prefixes,
+                        void* d_bins, size_t bins_bytes, void* d_ws, size_t ws_bytes) {
     if (!out) return SINET_E_INVAL;
     *out = nullptr;
     sinet_ctx* c = new (std::nothrow) sinet_ctx();
@@ -411,7 +417,7 @@ int sinet_open(sinet_ctx** out, const sinet_config* cfg, const uint32_t* prefix_
     auto bail = [&](int code) { delete c; return code; };
     Geometry g;
     if (!check_cfg(cfg, &c->err, &g)) { std::fprintf(stderr, "sinet_open: %s\n", c->err.c_str()); return bail(SINET_E_INVAL); }
-    if (!compile_prefixes(prefix_net, prefix_len, n_prefixes, &c->table, &c->err)) {
+    if (!compile_prefixes_labelled(prefix_net, prefix_len, prefix_label, n_prefixes, &c->table, &c->err)) {
         std::fprintf(stderr, "sinet_open: %s\n", c->err.c_str());
         return bail(SINET_E_INVAL);
     }
@@ -815,9 +821,14 @@ int sinet_read_totals(sinet_ctx* c, sinet_totals* out) {
 
 int sinet_table_member_host(const uint32_t* net, const uint8_t* len, uint32_t np,
                             const uint32_t* ips, uint64_t n, uint8_t* out) {
+    return sinet_table_member_host_labelled(net, len, nullptr, np, ips, n, out);
+}
+
+int sinet_table_member_host_labelled(const uint32_t* net, const uint8_t* len, const uint8_t* label, uint32_t np,
+                                     const uint32_t* ips, uint64_t n, uint8_t* out) {
     CompiledTable t;
     std::string err;
-    if (!compile_prefixes(net, len, np, &t, &err)) return SINET_E_INVAL;
+    if (!compile_prefixes_labelled(net, len, label, np, &t, &err)) return SINET_E_INVAL;
     if (n && (!ips || !out)) return SINET_E_INVAL;
     for (uint64_t i = 0; i < n; ++i) {
         // the kernels' lookup (sinet_device.cuh member()), evaluated on the host

@@ -51,7 +51,7 @@ class SinetHistogram:
 
     def __init__(self, nets, lens, window_start_ms: int, window_ms: int, bin_width_ms: int = 1,
                  lut=N.LUT_SRC_PRIORITY, device=None, rank: int = 0, world: int = 1,
-                 stream: torch.cuda.Stream | None = None, order: int = N.ORDER_AUTO):
+                 stream: torch.cuda.Stream | None = None, order: int = N.ORDER_AUTO, labels=None):
         if not torch.cuda.is_available():
             raise RuntimeError("SinetHistogram needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
@@ -80,9 +80,15 @@ class SinetHistogram:
             self.bins = torch.empty(bb // 8, dtype=torch.int64, device=self.device)
             self.ws = torch.empty(wb, dtype=torch.uint8, device=self.device)
         ctx = ctypes.c_void_p()
-        rc = lib.sinet_open(ctypes.byref(ctx), ctypes.byref(cfg), nets.ctypes.data_as(ctypes.c_void_p),
-                            lens.ctypes.data_as(ctypes.c_void_p), len(nets), _ptr(self.bins), bb,
-                            _ptr(self.ws), wb)
+        if labels is not None:   # NEXT-4: labelled longest-prefix match
+            labs = np.ascontiguousarray(np.asarray(labels, dtype=np.uint8))
+            assert labs.shape == nets.shape
+            lab_p = labs.ctypes.data_as(ctypes.c_void_p)
+        else:
+            lab_p = None
+        rc = lib.sinet_open_labelled(ctypes.byref(ctx), ctypes.byref(cfg), nets.ctypes.data_as(ctypes.c_void_p),
+                                     lens.ctypes.data_as(ctypes.c_void_p), lab_p, len(nets), _ptr(self.bins), bb,
+                                     _ptr(self.ws), wb)
         check(rc, None, "sinet_open")
         self.ctx = ctx
         self._staging = None
@@ -288,14 +294,16 @@ def exchange_plan(world: int, rank: int, nbins: int, nbins_pad: int, touched):
     return send.reshape(world, 2).astype(np.int64), recv.reshape(world, 2).astype(np.int64)
 
 
-def table_member_host(nets, lens, ips) -> np.ndarray:
+def table_member_host(nets, lens, ips, labels=None) -> np.ndarray:
     """Host evaluation of the compiled lookup table (prefix compiler check, no GPU)."""
     nets = np.ascontiguousarray(np.asarray(nets, dtype=np.uint32))
     lens = np.ascontiguousarray(np.asarray(lens, dtype=np.uint8))
     ips = np.ascontiguousarray(np.asarray(ips, dtype=np.uint32))
     out = np.empty(len(ips), dtype=np.uint8)
-    rc = lib.sinet_table_member_host(nets.ctypes.data_as(ctypes.c_void_p), lens.ctypes.data_as(ctypes.c_void_p),
-                                     len(nets), ips.ctypes.data_as(ctypes.c_void_p), len(ips),
-                                     out.ctypes.data_as(ctypes.c_void_p))
+    labs = None if labels is None else np.ascontiguousarray(np.asarray(labels, dtype=np.uint8))
+    rc = lib.sinet_table_member_host_labelled(
+        nets.ctypes.data_as(ctypes.c_void_p), lens.ctypes.data_as(ctypes.c_void_p),
+        None if labs is None else labs.ctypes.data_as(ctypes.c_void_p), len(nets),
+        ips.ctypes.data_as(ctypes.c_void_p), len(ips), out.ctypes.data_as(ctypes.c_void_p))
     check(rc, None, "table_member_host")
     return out

@@ -438,3 +438,23 @@ def test_full_size_sampled_parity(S, oracle_lib, name):
     got = bv[pick].cpu().numpy().view(np.uint64)
     np.testing.assert_array_equal(got[:, :, 0].T, o.count[:, p])
     np.testing.assert_array_equal(got[:, :, 1].T, o.bytes[:, p])
+
+
+# ----------------------------------------------------------------------------- NEXT-4 labelled LPM
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_labelled_lpm_parity(S, oracle_lib, strategy):
+    """C5-shaped table (4096 nested /8-/32 entries) with 30 % carve-outs: longest match decides."""
+    wl = WORKLOADS["c5"].with_(n=500_000, window_ms=3_600_000)
+    nets, lens = prefix_table(wl)
+    labels = (np.random.default_rng(5).random(len(nets)) < 0.7).astype(np.uint8)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram_lpm(*cols, nets, lens, labels, wl.window_start_ms, wl.window_ms, 1)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, order=strategy, labels=labels)
+    tg = torch.empty(wl.n, dtype=torch.uint8, device="cuda")
+    h.classify(*dev_cols(cols), tags=tg)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
+    t = tg.cpu().numpy()
+    np.testing.assert_array_equal(t & 1, oracle_lib.member_lpm(cols[1], nets, lens, labels))
+    np.testing.assert_array_equal((t >> 1) & 1, oracle_lib.member_lpm(cols[2], nets, lens, labels))

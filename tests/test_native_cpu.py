@@ -126,3 +126,22 @@ def test_exchange_plan_edges():
     assert recv[2].tolist() == [0, 0] and recv[3].tolist() == [0, 0]   # empty / disjoint
     with pytest.raises(N.SinetError):
         exchange_plan(3, 0, 1000, 1024, t[:3])             # pad not a multiple of world
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_labelled_lpm_table_matches_oracle(oracle_lib, seed):
+    """NEXT-4: the labelled table compiled to member intervals == the oracle's literal LPM scan."""
+    rng = np.random.default_rng(seed)
+    from synth import WORKLOADS, prefix_table
+    nets, lens = prefix_table(WORKLOADS["c5"])          # nested /8-/32 entries
+    nets, lens = nets[:3000], lens[:3000]
+    labels = (rng.random(len(nets)) < 0.7).astype(np.uint8)
+    ips = np.concatenate([edge_addresses(nets, lens),
+                          rng.integers(0, 1 << 32, 30_000, dtype=np.uint64).astype(np.uint32)])
+    got = table_member_host(nets, lens, ips, labels)
+    np.testing.assert_array_equal(got, oracle_lib.member_lpm(ips, nets, lens, labels))
+    # duplicates: the last equal entry wins
+    n2 = np.array([ip_ for ip_ in (0x85000000, 0x85000000)], np.uint32)
+    l2 = np.array([8, 8], np.uint8)
+    assert table_member_host(n2, l2, [0x85010203], [1, 0]).tolist() == [0]
+    assert table_member_host(n2, l2, [0x85010203], [0, 1]).tolist() == [1]

@@ -364,3 +364,32 @@ def test_watched_histogram_equals_histogram_of_filtered(oracle_lib):
     np.testing.assert_array_equal(res.count, ref.count)
     np.testing.assert_array_equal(res.totals, ref.totals)
     assert int(res.m_count.sum()) == int(m.sum())
+
+
+# ----------------------------------------------------------------------------- NEXT-4 labelled LPM
+def test_lpm_worked_values_and_bruteforce(oracle_lib):
+    nets = [ip("133.0.0.0"), ip("133.11.0.0"), ip("133.11.7.0"), ip("133.11.7.128")]
+    lens = [8, 16, 24, 25]
+    labs = [1, 0, 1, 0]          # 133/8 in, carve out 133.11/16, re-include 133.11.7/24, carve .128/25
+    cases = {"133.1.2.3": 1, "133.11.2.3": 0, "133.11.7.5": 1, "133.11.7.200": 0, "8.8.8.8": 0}
+    got = oracle_lib.member_lpm([ip(k) for k in cases], nets, lens, labs)
+    assert got.tolist() == list(cases.values())
+    # all labels 1 -> plain match-any membership (Alg. 1 over the list)
+    rnd = random.Random(26)
+    for _ in range(3000):
+        a, n2, l2 = _random_case(rnd)
+        lab = [rnd.randint(0, 1) for _ in n2]
+        assert oracle_lib.member_lpm([a], n2, l2, [1] * len(n2))[0] == oracle_lib.member(a, n2, l2)
+        assert bool(oracle_lib.member_lpm([a], n2, l2, lab)[0]) == brute.member_lpm_bitstring(a, n2, l2, lab)
+
+
+def test_histogram_members_equals_histogram_when_all_inside(oracle_lib):
+    # with every label 1 the LPM histogram is the plain histogram (same definition, given memberships)
+    wl, nets, lens, rec = _c1_small(60_000)
+    cols = to_numpy(rec)
+    a = _run(oracle_lib, wl, nets, lens, cols)
+    b = oracle_lib.classify_histogram_lpm(*cols, nets, lens, np.ones(len(nets), np.uint8), wl.window_start_ms,
+                                          wl.window_ms, 1)
+    np.testing.assert_array_equal(a.count, b.count)
+    np.testing.assert_array_equal(a.bytes, b.bytes)
+    np.testing.assert_array_equal(a.totals, b.totals)
