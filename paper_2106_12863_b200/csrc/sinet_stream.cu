@@ -231,14 +231,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t t = t_from + k;
             if (!touched(t)) continue;
             const uint32_t st = s_state[t & (NT - 1)];
-            if (((st >> 2) != t + 1u) || (st & 3u) == kBusy) busy = true;
-        }
-        for (uint32_t k = 0; k < nt; ++k) {
-            const uint32_t t = t_from + k;
-            if (!touched(t)) continue;
-            const uint32_t st = s_state[t & (NT - 1)];
             const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
-            if (o == kBusy) continue;
+            if (o == kBusy) { busy = true; continue; }
             for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin(t * kTileBins + i, o == kWon);
         }
         group_sync();
@@ -385,6 +379,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                 s_wtot[w][8] += o[0]; s_wtot[w][9] += o[1]; s_wtot[w][10] += o[2]; s_wtot[w][11] += o[3];
             }
         }
+        // Accumulate before the barrier every record whose tile is resident and neither being
+        // retired ([lo_t, act_t), claimed after the previous chunk) nor about to be recycled
+        // (>= lo_t + NT): retire only touches the slots of [lo_t, act_t).  Warps do this work
+        // instead of waiting at the barrier; the rest is accumulated after the retire.
+        bool done4[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) done4[j] = false;
+        if (!kAgg && have_window) {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j)
+                if (binned4[j] && bin4[j] / kTileBins - act_t < lo_t + NT - act_t) {
+                    accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
+                    done4[j] = true;
+                }
+        }
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
         if (lane == 0) { s_red[parity][0][warp] = bmin; s_red[parity][1][warp] = bmax; }
@@ -424,11 +433,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (!kAgg && all_in) {
 #pragma unroll
             for (int j = 0; j < RPT; ++j)
-                if (binned4[j]) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
+                if (binned4[j] && !done4[j]) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
         } else
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const bool b = binned4[j];
+            const bool b = binned4[j] && !done4[j];
             bool act = b;
             uint32_t cnt = 1u;
             uint64_t byt = cur.by[j];
