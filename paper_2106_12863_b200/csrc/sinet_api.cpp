@@ -651,8 +651,11 @@ int sinet_reduce(sinet_ctx* c) {
     if (!c) return SINET_E_INVAL;
     if (c->reduced) return fail(c, SINET_E_STATE, "already reduced: call sinet_reset first");
     DeviceGuard dg(c->device);
-    int rc = do_materialize(c);
-    if (rc) return rc;
+    const bool may_sparse = c->cfg.world > 1 && c->comm && c->exchange != 1 && c->ws.staging_bytes;
+    if (!may_sparse) {
+        int rc = do_materialize(c);
+        if (rc) return rc;
+    }
     if (c->cfg.world > 1 || c->comm) {
         if (!c->comm) return fail(c, SINET_E_NCCL, "no communicator: call sinet_comm_init");
         NcclApi* api = nccl_api(&c->err);
@@ -682,7 +685,26 @@ int sinet_reduce(sinet_ctx* c) {
             const uint64_t dense_moved = (uint64_t)(world - 1) * (c->geo.B_pad / (uint64_t)world) * (uint64_t)world;
             sparse = (c->exchange == 2 || total_moved * 2 <= dense_moved) &&
                      worst_recv * 32u <= (uint64_t)c->ws.staging_bytes;
-            if (sparse) plan_exchange(world, rank, c->geo.B, c->geo.B_pad, h.data(), &sd, &rv);
+            if (sparse) {
+                plan_exchange(world, rank, c->geo.B, c->geo.B_pad, h.data(), &sd, &rv);
+                // materialise only the owned slice and the slices sent (others stay virtual)
+                const uint64_t per = c->geo.B_pad / (uint64_t)world;
+                auto mat = [&](uint64_t b_lo, uint64_t b_n) -> int {
+                    if (!b_n) return SINET_OK;
+                    const uint32_t t0 = (uint32_t)(b_lo / kTileBins);
+                    const uint32_t t1 = (uint32_t)((b_lo + b_n + kTileBins - 1) / kTileBins);
+                    SINET_CUDA(c, launch_materialize_range(c->bins, ws_u32(c, c->ws.flags), t0, t1, init_word(c),
+                                                           c->materialize_grid, c->stream));
+                    c->launches++;
+                    return SINET_OK;
+                };
+                int mrc = mat(per * (uint64_t)rank, per);
+                for (int o = 0; o < world && !mrc; ++o) mrc = mat(sd[o].first, sd[o].n);
+                if (mrc) return mrc;
+            } else {
+                int rc = do_materialize(c);
+                if (rc) return rc;
+            }
         }
         ncclResult_t r = api->GroupStart();
         if (sparse) {

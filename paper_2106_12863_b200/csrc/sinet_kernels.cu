@@ -87,11 +87,19 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32_t n_tiles,
                                uint32_t init_word, int grid, cudaStream_t st) {
-    if (n_tiles == 0) return cudaSuccess;
-    uint32_t need = (n_tiles + 255u) / 256u;   // 8 warps x 32 tiles per block per step
+    return launch_materialize_range(bins, flags, 0, n_tiles, init_word, grid, st);
+}
+
+// tiles [t_lo, t_hi) only (the sparse multi-GPU merge materialises what it sends and owns)
+cudaError_t launch_materialize_range(unsigned long long* bins, uint32_t* flags, uint32_t t_lo, uint32_t t_hi,
+                                     uint32_t init_word, int grid, cudaStream_t st) {
+    if (t_hi <= t_lo) return cudaSuccess;
+    const uint32_t n = t_hi - t_lo;
+    uint32_t need = (n + 255u) / 256u;   // 8 warps x 32 tiles per block per step
     int g = (int)((need < (uint32_t)grid) ? need : (uint32_t)grid);
     if (g < 1) g = 1;
-    k_materialize<<<g, 256, 0, st>>>(reinterpret_cast<ulonglong2*>(bins), flags, n_tiles, init_word);
+    k_materialize<<<g, 256, 0, st>>>(reinterpret_cast<ulonglong2*>(bins) + (size_t)t_lo * kTileBins * 2u,
+                                     flags + t_lo, n, init_word);
     return cudaGetLastError();
 }
 

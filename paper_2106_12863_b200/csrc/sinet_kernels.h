@@ -10,6 +10,8 @@ namespace sinet {
 
 cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32_t n_tiles,
                                uint32_t init_word, int grid, cudaStream_t st);
+cudaError_t launch_materialize_range(unsigned long long* bins, uint32_t* flags, uint32_t t_lo, uint32_t t_hi,
+                                     uint32_t init_word, int grid, cudaStream_t st);
 
 cudaError_t setup_hist_atomic();
 int hist_atomic_blocks_per_sm(const KernelParams& p);
