@@ -406,6 +406,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         const bool any = bmin <= bmax;
         const uint32_t bmin_t = bmin / kTileBins, bmax_t = bmax / kTileBins;
 
+        // every tile this chunk reaches at or above the claim boundary joins the hull now,
+        // before any retire: tiles that received pre-barrier accumulation must be seen as
+        // touched by an emergency retire below (tiles in [lo_t, act_t) were claimed already)
+        if (any) { gmin = min(gmin, bmin); gmax = max(gmax, bmax); }
+        if (any && have_window) {
+            hull_lo = min(hull_lo, bmin_t > act_t ? bmin_t : act_t);
+            hull_hi = max(hull_hi, bmax_t);
+        }
+
         // ---- a6 (retire): tiles claimed after the previous chunk
         retire(lo_t, act_t);
         lo_t = act_t;
@@ -413,17 +422,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             if (!have_window) {
                 have_window = true;
                 lo_t = act_t = (bmax_t - bmin_t >= NT) ? bmax_t - NT + 1u : bmin_t;
+                hull_lo = min(hull_lo, bmin_t > lo_t ? bmin_t : lo_t);
+                hull_hi = max(hull_hi, bmax_t);
             } else if (bmax_t >= lo_t + NT) {   // the chunk reaches past the ring: retire now
                 const uint32_t nlo = bmax_t - NT + 1u;
                 claim_and_retire(lo_t, (nlo - lo_t < NT) ? nlo : lo_t + NT);
                 lo_t = act_t = nlo;
             }
-        }
-
-        if (any) { gmin = min(gmin, bmin); gmax = max(gmax, bmax); }
-        if (any) {   // every resident tile this chunk reaches joins the hull
-            hull_lo = min(hull_lo, bmin_t > lo_t ? bmin_t : lo_t);
-            hull_hi = max(hull_hi, bmax_t);
         }
         const bool key32 = p.nbins < 0x40000000u;   // keys 2*bin+dir stay below the lane sentinels
 
