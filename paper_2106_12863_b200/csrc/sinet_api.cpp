@@ -154,6 +154,7 @@ struct sinet_ctx {
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t ranges_per_group = 0;
     uint32_t stream_threads = 0;
+    uint32_t pf_chunks = 2;
     int exchange = 0;             // multi-GPU merge: 0 auto (sparse when cheaper), 1 dense, 2 sparse
     int last_exchange = 0;        // 1 dense reduce-scatter, 2 sparse touched-range exchange
     // NEXT-2 watchlist (caller-owned device buffer)
@@ -222,6 +223,7 @@ KernelParams base_params(sinet_ctx* c) {
     p.stream_groups = c->stream_groups;
     p.ranges_per_group = c->ranges_per_group;
     p.stream_threads = c->stream_threads;
+    p.pf_chunks = c->pf_chunks;
     p.range_counter = ws_u32(c, c->ws.counters);
     p.touched = ws_u32(c, c->ws.counters) + 4;
     p.wbits = c->wbits;
@@ -450,6 +452,7 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
     if (const char* r = std::getenv("SINET_RANGES")) c->ranges_per_group = (uint32_t)std::atoi(r);
     if (const char* t = std::getenv("SINET_STREAM_THREADS")) c->stream_threads = (uint32_t)std::atoi(t);
     if (const char* x = std::getenv("SINET_EXCHANGE")) c->exchange = std::atoi(x);
+    if (const char* f = std::getenv("SINET_PF")) c->pf_chunks = (uint32_t)std::atoi(f);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states

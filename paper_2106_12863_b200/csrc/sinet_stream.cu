@@ -34,6 +34,25 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     return v;
 }
 
+// TMA bulk prefetch of [ptr, ptr + bytes) into L2 (16-byte aligned, multiple of 16; a hint)
+__device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
+// Prefetch the four columns of virtual records [v0, v1) into L2 (clamped to the batch).
+__device__ __forceinline__ void prefetch_records(const KernelParams& p, uint64_t v0, uint64_t v1) {
+    if (v0 < p.head) v0 = p.head;
+    if (v1 > p.nv) v1 = p.nv;
+    v0 = (v0 + 3) & ~3ull;   // whole 16-byte groups only (the virtual index is 16-byte aligned per 4)
+    v1 &= ~3ull;
+    if (v1 <= v0) return;
+    const uint64_t a = v0 - p.head, n = v1 - v0;
+    prefetch_l2(p.ts + a, (uint32_t)(n * 8));
+    prefetch_l2(p.src + a, (uint32_t)(n * 4));
+    prefetch_l2(p.dst + a, (uint32_t)(n * 4));
+    prefetch_l2(p.bytes + a, (uint32_t)(n * 8));
+}
+
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -315,6 +334,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     const uint64_t full_hi = (r1 > p.nv) ? r1 - 4 : r1;
     constexpr uint64_t CH = (uint64_t)GT * RPT;   // records per chunk
     Rec cur, nxt;
+    const uint64_t kPF = p.pf_chunks;   // L2 prefetch distance in chunks (0: off)
+    if (tid == 0 && kPF > 1) prefetch_records(p, r0 + CH, min(r0 + kPF * CH, r1));
     if (r0 + (uint64_t)tid * RPT < r1) loadN<RPT>(p, r0 + (uint64_t)tid * RPT, cur);
     uint32_t parity = 0;
 
@@ -324,7 +345,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         // every record of the chunk valid (all but the batch's ragged ends): no per-record checks
         const bool full = cbase >= full_lo && cbase + CH <= full_hi;
         const bool tags_on = p.tags != nullptr;
-        if (my_v + CH < r1) loadN<RPT>(p, my_v + CH, nxt);   // prefetch
+        if (my_v + CH < r1) loadN<RPT>(p, my_v + CH, nxt);   // prefetch into registers
+        // keep more bytes in flight than one chunk of registers: the chunks kPF ahead go to L2
+        if (tid == 0 && kPF && cbase + kPF * CH < r1) prefetch_records(p, cbase + kPF * CH, min(cbase + (kPF + 1) * CH, r1));
 
         // ---- a3-a5: classify and map this chunk (the claims issued last chunk resolve meanwhile)
         uint32_t bin4[RPT], dir4[RPT];
