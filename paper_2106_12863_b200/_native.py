@@ -13,8 +13,14 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libsinet.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "sinet.h")
 
-if not os.path.exists(LIB_PATH):
-    raise ImportError(f"libsinet.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+if not os.path.exists(LIB_PATH) or os.environ.get("SINET_REBUILD") == "1":
+    # Compile the CUDA library in-tree (nvcc, sm_100a); never substitute anything for it.
+    from . import _build
+    try:
+        _build.build()
+    except Exception as e:  # noqa: BLE001
+        raise ImportError(f"libsinet.so not built at {LIB_PATH} and nvcc build failed ({e}): "
+                          "run `python -c 'import __graft_entry__ as g; g.build()'`") from e
 
 lib = ctypes.CDLL(LIB_PATH)
 
