@@ -74,3 +74,62 @@ def member_lpm_bitstring(ip: int, nets, lens, labels) -> bool:
         if s[:z] == bits32(int(n))[:z] and z >= best:
             best, lab = z, bool(l)
     return lab
+
+
+# ----------------------------------------------------------------------------- NEXT-3
+_TIME_RE = None
+
+
+def parse_line_python(line: bytes, tz_offset_min: int = 0):
+    """PA-7080 line (Table 1) by Python's own libraries: str.split, a regular
+    expression for the capture_time shape, datetime (calendar validity), calendar.timegm
+    (epoch seconds), ipaddress.IPv4Address (dotted quad), int() (bytes).  Returns
+    (status, ts_ms, src, dst, bytes) with the status codes of oracle/core.py."""
+    import calendar
+    import datetime
+    import re
+    global _TIME_RE
+    if _TIME_RE is None:
+        _TIME_RE = re.compile(rb"(\d{4})/(\d{2})/(\d{2}) (\d{2}):(\d{2}):(\d{2})\.(\d{3})")
+    if len(line) > 2047:
+        return 1, 0, 0, 0, 0
+    if line.endswith(b"\r"):
+        line = line[:-1]
+    f = line.split(b",")
+    if len(f) != 24:
+        return 2, 0, 0, 0, 0
+    m = _TIME_RE.fullmatch(f[0])
+    ts = None
+    if m:
+        try:
+            Y, M, D, h, mi, s, ms = (int(x) for x in m.groups())
+            dt = datetime.datetime(Y, M, D, h, mi, s)
+            if Y >= 1970:
+                ts = (calendar.timegm(dt.timetuple()) * 1000 + ms) - tz_offset_min * 60000
+                if ts < 0:
+                    ts = None
+        except ValueError:
+            ts = None
+    if ts is None:
+        return 3, 0, 0, 0, 0
+    ips = []
+    for k, code in ((4, 4), (7, 5)):
+        try:
+            txt = f[k].decode("ascii")
+            if not all(c in "0123456789." for c in txt):
+                raise ValueError
+            ips.append(int(ipaddress.IPv4Address(txt)))
+        except (ValueError, UnicodeDecodeError):
+            return code, 0, 0, 0, 0
+    b = f[20]
+    if not (1 <= len(b) <= 20 and all(48 <= c <= 57 for c in b)) or int(b) > M64:
+        return 6, 0, 0, 0, 0
+    return 0, ts, ips[0], ips[1], int(b)
+
+
+def parse_text_python(text: bytes, tz_offset_min: int = 0):
+    """Lines = text.split(b"\\n") without the empty piece after a final newline."""
+    lines = text.split(b"\n")
+    if lines and lines[-1] == b"":
+        lines.pop()
+    return [parse_line_python(l, tz_offset_min) for l in lines]

@@ -70,6 +70,12 @@ def _load():
         lib.oracle_sparse.argtypes = [u64p, u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                       u64p, u64p, u64p, ctypes.c_uint64]
         lib.oracle_sparse.restype = ctypes.c_uint64
+        lib.oracle_parse_text.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int32, u64p, u32p, u32p,
+                                          u64p, u8p, u64p]
+        lib.oracle_parse_text.restype = None
+        lib.oracle_parse_line.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int32, u64p, u32p, u32p,
+                                          u64p]
+        lib.oracle_parse_line.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -234,3 +240,47 @@ def classify_histogram_lpm(ts, src, dst, nbytes, nets, lens, labels, start, wind
                                      _ptr(lut_a, ctypes.c_uint8), _ptr(res.count, ctypes.c_uint64),
                                      _ptr(res.bytes, ctypes.c_uint64), _ptr(res.totals, ctypes.c_uint64))
     return res
+
+
+# NEXT-3 line status codes (readings A27-A31)
+PARSE_OK, PARSE_LONG, PARSE_COLUMNS, PARSE_TIME, PARSE_SRC, PARSE_DST, PARSE_BYTES = range(7)
+
+
+class ParseResult:
+    def __init__(self, ts, src, dst, nbytes, status):
+        self.ts, self.src, self.dst, self.bytes, self.status = ts, src, dst, nbytes, status
+
+    @property
+    def n_lines(self):
+        return len(self.status)
+
+    @property
+    def n_valid(self):
+        return len(self.ts)
+
+
+def parse_text(text: bytes, tz_offset_min: int = 0) -> ParseResult:
+    """NEXT-3: PA-7080 session-log text (Table 1) -> (ts, src, dst, bytes) of the
+    valid lines in line order + a status per line."""
+    text = bytes(text)
+    cap = text.count(b"\n") + 1
+    ts = np.zeros(cap, np.uint64)
+    src = np.zeros(cap, np.uint32)
+    dst = np.zeros(cap, np.uint32)
+    nb = np.zeros(cap, np.uint64)
+    st = np.zeros(cap, np.uint8)
+    out = np.zeros(2, np.uint64)
+    _load().oracle_parse_text(text, len(text), tz_offset_min, _ptr(ts, ctypes.c_uint64), _ptr(src, ctypes.c_uint32),
+                              _ptr(dst, ctypes.c_uint32), _ptr(nb, ctypes.c_uint64), _ptr(st, ctypes.c_uint8),
+                              _ptr(out, ctypes.c_uint64))
+    n, v = int(out[0]), int(out[1])
+    return ParseResult(ts[:v], src[:v], dst[:v], nb[:v], st[:n])
+
+
+def parse_line(line: bytes, tz_offset_min: int = 0):
+    """One line's (status, ts, src, dst, bytes)."""
+    ts, nb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    s, d = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    st = _load().oracle_parse_line(bytes(line), len(line), tz_offset_min, ctypes.byref(ts), ctypes.byref(s),
+                                   ctypes.byref(d), ctypes.byref(nb))
+    return st, ts.value, s.value, d.value, nb.value

@@ -320,3 +320,176 @@ void oracle_histogram_members(const uint64_t* ts, const uint8_t* s_in, const uin
         out_bytes[(uint64_t)dir * nbins + key] += bytes[r];
     }
 }
+
+/* ---------------------------------------------------------------------- */
+/* NEXT-3: session-log text -> the four columns the path reads.
+ *
+ * Table 1 ("PA-7080 data description") lists the 24 items of a
+ * session record in order; the path needs No. 1 capture_time,
+ * No. 5 source_ip, No. 8 destination_ip and No. 21 bytes
+ * (P:L254).  The paper prints no file syntax; readings A27-A31
+ * fix it: one record per line, '\n' separated (an optional '\r' before it is
+ * dropped), 24 comma-separated fields in Table 1 order, capture_time as
+ * "YYYY/MM/DD HH:MM:SS.mmm" (Table 1's sample value) in local time at
+ * tz_offset_min minutes east of UTC, dotted-quad IPv4 addresses
+ * ("translated to a 32-bit sequence"; first octet most
+ * significant), bytes a decimal u64.  Other fields are opaque.
+ *
+ * Status per line (first failing check wins, in this order):
+ *   0 OK, 1 LONG (content > 2047 bytes), 2 COLUMNS (not 24 fields),
+ *   3 TIME, 4 SRC, 5 DST, 6 BYTES.
+ * Valid lines are written to the output columns in line order (skip policy);
+ * every line, valid or not, gets a status and a line number.
+ *
+ * Written as plain string handling: find the line, split it on every comma,
+ * then parse the four fields character by character.                       */
+
+#define ORACLE_PARSE_MAX_LINE 2047u
+
+static int oracle_is_leap(uint32_t y)
+{
+    return (y % 4u == 0u && y % 100u != 0u) || y % 400u == 0u;
+}
+
+static uint32_t oracle_month_days(uint32_t y, uint32_t m)
+{
+    static const uint32_t days[12] = {31, 28, 31, 30, 31, 30, 31, 31, 30, 31, 30, 31};
+    return (m == 2u && oracle_is_leap(y)) ? 29u : days[m - 1u];
+}
+
+/* Reads exactly k decimal digits at s into *v; 0 if any is not a digit. */
+static int oracle_digits(const char* s, uint32_t k, uint32_t* v)
+{
+    uint32_t x = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+        if (s[i] < '0' || s[i] > '9') return 0;
+        x = x * 10u + (uint32_t)(s[i] - '0');
+    }
+    *v = x;
+    return 1;
+}
+
+/* capture_time "YYYY/MM/DD HH:MM:SS.mmm" -> epoch ms (UTC) of that local time.
+ * Days since 1970-01-01 are counted year by year and month by month (the
+ * Gregorian calendar; Unix time has no leap seconds, reading A11).         */
+int oracle_parse_time(const char* f, uint64_t len, int32_t tz_offset_min, uint64_t* out)
+{
+    uint32_t Y, M, D, h, mi, s, ms;
+    if (len != 23u) return 0;
+    if (f[4] != '/' || f[7] != '/' || f[10] != ' ' || f[13] != ':' || f[16] != ':' || f[19] != '.')
+        return 0;
+    if (!oracle_digits(f + 0, 4, &Y) || !oracle_digits(f + 5, 2, &M) || !oracle_digits(f + 8, 2, &D) ||
+        !oracle_digits(f + 11, 2, &h) || !oracle_digits(f + 14, 2, &mi) ||
+        !oracle_digits(f + 17, 2, &s) || !oracle_digits(f + 20, 3, &ms))
+        return 0;
+    if (Y < 1970u || M < 1u || M > 12u || D < 1u || D > oracle_month_days(Y, M)) return 0;
+    if (h > 23u || mi > 59u || s > 59u) return 0;
+    uint64_t days = 0;
+    for (uint32_t y = 1970u; y < Y; ++y) days += oracle_is_leap(y) ? 366u : 365u;
+    for (uint32_t m = 1u; m < M; ++m) days += oracle_month_days(Y, m);
+    days += D - 1u;
+    int64_t local_ms = (int64_t)((((days * 24u + h) * 60u + mi) * 60u + s) * 1000u + ms);
+    int64_t utc_ms = local_ms - (int64_t)tz_offset_min * 60000;
+    if (utc_ms < 0) return 0;
+    *out = (uint64_t)utc_ms;
+    return 1;
+}
+
+/* Dotted quad: four octets of 1-3 decimal digits, no leading zero unless the
+ * octet is "0", each <= 255 (the strictness of Python's ipaddress module). */
+int oracle_parse_ipv4(const char* f, uint64_t len, uint32_t* out)
+{
+    uint32_t value = 0, octets = 0;
+    uint64_t i = 0;
+    while (octets < 4u) {
+        uint64_t b = i;
+        uint32_t x = 0;
+        while (i < len && f[i] >= '0' && f[i] <= '9') {
+            x = x * 10u + (uint32_t)(f[i] - '0');
+            ++i;
+            if (i - b > 3u) return 0;
+        }
+        uint64_t nd = i - b;
+        if (nd == 0u || x > 255u || (nd > 1u && f[b] == '0')) return 0;
+        value = (value << 8) | x;
+        ++octets;
+        if (octets < 4u) {
+            if (i >= len || f[i] != '.') return 0;
+            ++i;
+        }
+    }
+    if (i != len) return 0;
+    *out = value;
+    return 1;
+}
+
+/* bytes: 1 to 20 decimal digits, value < 2^64 ("NA" is an error, reading A30). */
+int oracle_parse_u64(const char* f, uint64_t len, uint64_t* out)
+{
+    if (len == 0u || len > 20u) return 0;
+    uint64_t x = 0;
+    for (uint64_t i = 0; i < len; ++i) {
+        if (f[i] < '0' || f[i] > '9') return 0;
+        uint64_t d = (uint64_t)(f[i] - '0');
+        if (x > (UINT64_MAX - d) / 10u) return 0;   /* x*10 + d would exceed 2^64 - 1 */
+        x = x * 10u + d;
+    }
+    *out = x;
+    return 1;
+}
+
+/* One line (content without its '\n'): status code, and on OK the four values. */
+int oracle_parse_line(const char* line, uint64_t len, int32_t tz_offset_min,
+                      uint64_t* ts, uint32_t* src, uint32_t* dst, uint64_t* bytes)
+{
+    if (len > ORACLE_PARSE_MAX_LINE) return 1;
+    if (len > 0u && line[len - 1u] == '\r') --len;
+    uint64_t fb[24], fe[24];           /* field i = line[fb[i], fe[i]) */
+    uint32_t nf = 0;
+    uint64_t b = 0;
+    for (uint64_t i = 0; i <= len; ++i) {
+        if (i == len || line[i] == ',') {
+            if (nf == 24u) return 2;    /* a 25th field */
+            fb[nf] = b;
+            fe[nf] = i;
+            ++nf;
+            b = i + 1u;
+        }
+    }
+    if (nf != 24u) return 2;
+    /* Table 1 numbering is 1-based: No. 1, 5, 8, 21 are fields 0, 4, 7, 20. */
+    if (!oracle_parse_time(line + fb[0], fe[0] - fb[0], tz_offset_min, ts)) return 3;
+    if (!oracle_parse_ipv4(line + fb[4], fe[4] - fb[4], src)) return 4;
+    if (!oracle_parse_ipv4(line + fb[7], fe[7] - fb[7], dst)) return 5;
+    if (!oracle_parse_u64(line + fb[20], fe[20] - fb[20], bytes)) return 6;
+    return 0;
+}
+
+/* The whole text: a line starts at offset 0 and after every '\n' that is not
+ * the last byte (so "" has no line and a final '\n' ends the last line).
+ * status may be NULL; out[0] = lines, out[1] = valid lines.                 */
+void oracle_parse_text(const char* text, uint64_t len, int32_t tz_offset_min,
+                       uint64_t* ts, uint32_t* src, uint32_t* dst, uint64_t* bytes,
+                       uint8_t* status, uint64_t* out)
+{
+    uint64_t lines = 0, valid = 0, start = 0;
+    while (start < len) {
+        uint64_t end = start;
+        while (end < len && text[end] != '\n') ++end;
+        uint64_t t = 0, b = 0;
+        uint32_t s = 0, d = 0;
+        int st = oracle_parse_line(text + start, end - start, tz_offset_min, &t, &s, &d, &b);
+        if (status) status[lines] = (uint8_t)st;
+        if (st == 0) {
+            ts[valid] = t;
+            src[valid] = s;
+            dst[valid] = d;
+            bytes[valid] = b;
+            ++valid;
+        }
+        ++lines;
+        start = end + 1u;
+    }
+    out[0] = lines;
+    out[1] = valid;
+}
