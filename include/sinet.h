@@ -266,6 +266,63 @@ int sinet_export_sparse(sinet_ctx* ctx, int dir, uint64_t* d_ts_ms, uint64_t* d_
 /* Copy the totals to host (synchronises the stream). */
 int sinet_read_totals(sinet_ctx* ctx, sinet_totals* out);
 
+/* ---------------------------------------------------------------- NEXT-3: session-log text
+ * The step before the path: PA-7080 session-log text (Table 1) into
+ * the four device columns sinet_classify_histogram reads.  The paper prints the
+ * 24 items and sample values but no file syntax; readings A27-A31 fix it:
+ *   - one record per line, lines separated by '\n' (a '\r' before it is allowed);
+ *     a line starts at offset 0 and after every '\n' that is not the last byte;
+ *   - 24 comma-separated fields in Table 1 order; the parser reads No. 1
+ *     capture_time "YYYY/MM/DD HH:MM:SS.mmm" (local time at tz_offset_min minutes
+ *     east of UTC, Gregorian calendar, no leap seconds; result epoch ms UTC >= 0),
+ *     No. 5 source_ip and No. 8 destination_ip (dotted quad: four 1-3 digit octets
+ *     <= 255, no leading zeros), No. 21 bytes (1-20 decimal digits, < 2^64);
+ *     every other field is opaque;
+ *   - line status, the first failing check in this order: LONG (content, '\r'
+ *     included, longer than SINET_PARSE_MAX_LINE bytes), COLUMNS (not 24 fields),
+ *     TIME, SRC, DST, BYTES; else OK.
+ * Valid lines are written, in line order, to out (skip policy); the per-line
+ * status array and the counts let the caller apply any other policy. */
+#define SINET_PARSE_MAX_LINE 2047
+#define SINET_LINE_OK       0
+#define SINET_LINE_LONG     1
+#define SINET_LINE_COLUMNS  2
+#define SINET_LINE_TIME     3
+#define SINET_LINE_SRC      4
+#define SINET_LINE_DST      5
+#define SINET_LINE_BYTES    6
+
+/* Output columns of the parser (device pointers, naturally aligned; capacity records). */
+typedef struct {
+    uint64_t* ts_ms;
+    uint32_t* src;
+    uint32_t* dst;
+    uint64_t* bytes;
+    uint64_t capacity;
+} sinet_columns;
+
+typedef struct {
+    uint64_t lines;            /* lines in the text */
+    uint64_t valid;            /* lines with status OK (records produced; see E_RANGE) */
+    uint64_t first_bad_line;   /* 0-based index of the first non-OK line, UINT64_MAX if none */
+    uint64_t by_status[7];     /* lines per SINET_LINE_* code */
+} sinet_parse_result;
+
+/* Device workspace of sinet_parse_text for text_bytes of text (256-byte aligned). */
+size_t sinet_parse_workspace_bytes(uint64_t text_bytes);
+/* Parse d_text[0, text_bytes) (device, 16-byte aligned; not modified) into out;
+ * if d_status != NULL, d_status[i] = status of line i for i < status_capacity.
+ * Enqueued on `stream` (a cudaStream_t, NULL = legacy default); synchronises it
+ * to fill *result (host).  tz_offset_min in [-1440, 1440] (JST logs: 540).
+ * Errors: E_INVAL (NULL result, bad tz, workspace too small, NULL columns with
+ * capacity > 0); E_ALIGN (text or columns misaligned); E_RANGE (more valid lines
+ * than out.capacity: the first capacity records are written, result is complete);
+ * E_CUDA.  Detail string: sinet_parse_last_error() (per thread). */
+int sinet_parse_text(const uint8_t* d_text, uint64_t text_bytes, int32_t tz_offset_min,
+                     const sinet_columns* out, uint8_t* d_status, uint64_t status_capacity,
+                     void* d_ws, size_t ws_bytes, void* stream, sinet_parse_result* result);
+const char* sinet_parse_last_error(void);
+
 /* ---------------------------------------------------------------- introspection */
 const char* sinet_last_error(const sinet_ctx* ctx);
 /* Number of kernels this ctx has launched since open (all kinds). */

@@ -53,6 +53,18 @@ class Totals(ctypes.Structure):
                 ("oow_count", ctypes.c_uint64 * 2), ("oow_bytes", ctypes.c_uint64 * 2)]
 
 
+class Columns(ctypes.Structure):
+    _fields_ = [("ts_ms", ctypes.c_void_p), ("src", ctypes.c_void_p), ("dst", ctypes.c_void_p),
+                ("bytes", ctypes.c_void_p), ("capacity", ctypes.c_uint64)]
+
+
+class ParseResult(ctypes.Structure):
+    _fields_ = [("lines", ctypes.c_uint64), ("valid", ctypes.c_uint64), ("first_bad_line", ctypes.c_uint64),
+                ("by_status", ctypes.c_uint64 * 7)]
+
+
+LINE_OK, LINE_LONG, LINE_COLUMNS, LINE_TIME, LINE_SRC, LINE_DST, LINE_BYTES = range(7)
+
 _vp, _u64, _u32, _i = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
 _CP = ctypes.POINTER(Config)
 _SIGS = {
@@ -91,6 +103,10 @@ _SIGS = {
     "sinet_touched_range": ([_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u32)], _i),
     "sinet_exchange_plan": ([ctypes.c_int32, ctypes.c_int32, _u64, _u64, _vp, _vp, _vp], _i),
     "sinet_table_member_host": ([_vp, _vp, _u32, _vp, _u64, _vp], _i),
+    "sinet_parse_workspace_bytes": ([_u64], ctypes.c_size_t),
+    "sinet_parse_text": ([_vp, _u64, ctypes.c_int32, ctypes.POINTER(Columns), _vp, _u64, _vp, ctypes.c_size_t, _vp,
+                          ctypes.POINTER(ParseResult)], _i),
+    "sinet_parse_last_error": ([], ctypes.c_char_p),
     "sinet_table_member_host_labelled": ([_vp, _vp, _vp, _u32, _vp, _u64, _vp], _i),
 }
 for _name, (_args, _res) in _SIGS.items():

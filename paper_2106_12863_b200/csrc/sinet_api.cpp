@@ -15,6 +15,7 @@
 
 #include "prefix_compile.h"
 #include "sinet_kernels.h"
+#include "sinet_parse.h"
 
 using namespace sinet;
 
@@ -921,3 +922,82 @@ int sinet_kernel_time(sinet_ctx* c, double* total_ms, uint64_t* launches) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ NEXT-3: text parser
+namespace {
+thread_local std::string g_parse_err;
+int parse_fail(int code, const std::string& msg) {
+    g_parse_err = msg;
+    return code;
+}
+int parse_sm_count() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 1;
+}
+// workspace: ticket (8) + result (10 x 8) padded to 256, then two look-back arrays
+uint64_t parse_chunks(uint64_t text_bytes) { return (text_bytes + kParseChunk - 1) / kParseChunk; }
+}  // namespace
+
+extern "C" size_t sinet_parse_workspace_bytes(uint64_t text_bytes) {
+    return 256u + 16u * (size_t)parse_chunks(text_bytes);
+}
+
+extern "C" const char* sinet_parse_last_error(void) { return g_parse_err.c_str(); }
+
+extern "C" int sinet_parse_text(const uint8_t* d_text, uint64_t text_bytes, int32_t tz_offset_min,
+                                const sinet_columns* out, uint8_t* d_status, uint64_t status_capacity,
+                                void* d_ws, size_t ws_bytes, void* stream, sinet_parse_result* result) {
+    g_parse_err.clear();
+    if (!result || !out) return parse_fail(SINET_E_INVAL, "parse_text: NULL result or columns");
+    if (tz_offset_min < -1440 || tz_offset_min > 1440)
+        return parse_fail(SINET_E_INVAL, "parse_text: tz_offset_min outside [-1440, 1440]");
+    if (out->capacity && (!out->ts_ms || !out->src || !out->dst || !out->bytes))
+        return parse_fail(SINET_E_INVAL, "parse_text: NULL output column with capacity > 0");
+    if (text_bytes && !d_text) return parse_fail(SINET_E_INVAL, "parse_text: NULL text");
+    if (!d_ws || ws_bytes < sinet_parse_workspace_bytes(text_bytes) || (reinterpret_cast<uintptr_t>(d_ws) & 255u))
+        return parse_fail(SINET_E_INVAL, "parse_text: workspace missing, too small or not 256-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(d_text) & 15u) || (reinterpret_cast<uintptr_t>(out->ts_ms) & 7u) ||
+        (reinterpret_cast<uintptr_t>(out->bytes) & 7u) || (reinterpret_cast<uintptr_t>(out->src) & 3u) ||
+        (reinterpret_cast<uintptr_t>(out->dst) & 3u))
+        return parse_fail(SINET_E_ALIGN, "parse_text: text must be 16-byte aligned, columns naturally aligned");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t nch = parse_chunks(text_bytes);
+    uint8_t* ws = reinterpret_cast<uint8_t*>(d_ws);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 256u + 16u * (size_t)nch, st);
+    unsigned long long* res = reinterpret_cast<unsigned long long*>(ws + 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(res + 2, 0xFF, 8, st);   // first bad line: none
+    ParseParams p{};
+    p.text = d_text;
+    p.len = text_bytes;
+    p.tz_offset_min = tz_offset_min;
+    p.ts = out->ts_ms;
+    p.src = out->src;
+    p.dst = out->dst;
+    p.bytes = out->bytes;
+    p.cap = out->capacity;
+    p.status = d_status;
+    p.status_cap = d_status ? status_capacity : 0;
+    p.ticket = reinterpret_cast<unsigned long long*>(ws);
+    p.result = res;
+    p.st_lines = reinterpret_cast<unsigned long long*>(ws + 256);
+    p.st_valid = p.st_lines + nch;
+    p.n_chunks = nch;
+    if (e == cudaSuccess && nch) e = launch_parse_text(p, parse_sm_count(), st);
+    unsigned long long h[10] = {0};
+    unsigned long long last[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && nch) e = cudaMemcpyAsync(&last[0], p.st_lines + nch - 1, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && nch) e = cudaMemcpyAsync(&last[1], p.st_valid + nch - 1, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return parse_fail(SINET_E_CUDA, std::string("parse_text: ") + cudaGetErrorString(e));
+    const unsigned long long mask = (1ull << 62) - 1;
+    result->lines = last[0] & mask;         // the last chunk's inclusive prefix
+    result->valid = last[1] & mask;
+    result->first_bad_line = h[2];
+    for (int k = 0; k < 7; ++k) result->by_status[k] = h[3 + k];
+    if (result->valid > out->capacity)
+        return parse_fail(SINET_E_RANGE, "parse_text: more valid lines than out.capacity");
+    return SINET_OK;
+}

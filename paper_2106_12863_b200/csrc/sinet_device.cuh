@@ -46,6 +46,50 @@ __device__ __forceinline__ uint32_t member(uint32_t ip, const Table& T) {
     return cnt & 1u;
 }
 
+// member() for K addresses at once, with the same result per address.  The class word
+// and the rank of every address are loaded together (the rank's address depends on the ip
+// only), then every mixed block's /24 class, so a thread has K independent loads in flight
+// per level (2 dependent shared-memory round trips instead of 3 serial ones per address,
+// and no per-address branch).  Only addresses in a mixed /24 take the boundary search.
+template <int K>
+__device__ __forceinline__ void member_batch(const uint32_t (&ip)[K], uint32_t (&in)[K], const Table& T) {
+    uint32_t w[K], r[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        w[k] = T.cls2[ip[k] >> 20];
+        r[k] = T.rank[ip[k] >> 20];
+    }
+    uint32_t c2[K];
+    bool search = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t sh = ((ip[k] >> 16) & 15u) * 2u;
+        const uint32_t c = (w[k] >> sh) & 3u;
+        const uint32_t mixed = (w[k] >> 1) & ~w[k] & 0x55555555u;
+        r[k] += __popc(mixed & ((1u << sh) - 1u));     // index among the mixed blocks (if c == 2)
+        const uint32_t y = (ip[k] >> 8) & 0xFFu;
+        c2[k] = (c == 2u) ? ((T.l2[r[k] * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u) : c;
+        search |= c2[k] == 2u;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) in[k] = c2[k] & 1u;
+    if (search) {   // rare: a prefix longer than /24 shares this /24 with non-members
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (c2[k] != 2u) continue;
+            const uint32_t e = T.mentry[r[k]];
+            uint32_t cnt = e & 0xFFFFu, len = e >> 16;
+            const uint32_t* b = T.bnd + cnt;
+            while (len) {
+                const uint32_t half = len >> 1;
+                if (b[half] <= ip[k]) { b += half + 1; cnt += half + 1; len -= half + 1; }
+                else len = half;
+            }
+            in[k] = cnt & 1u;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- NEXT-2: watchlist predicate
 // Exact-address set (AbuseIPDB / GRIZZLY STEPPE lists): a /16 bitmap
 // rejects most addresses with one cached load, a binary search confirms the rest.
@@ -102,13 +146,16 @@ struct WarpTotals {
         ob[0] = ob[1] = 0ull;
     }
     __device__ __forceinline__ void add(bool valid, uint32_t cell, bool oow, uint32_t dir, uint64_t b) {
-        if (valid) {
-            const bool s = cell & 2u, d = cell & 1u;
-            cT += 1u; bT += b;
-            if (s) { cS += 1u; bS += b; }
-            if (d) { cD += 1u; bD += b; }
-            if (s && d) { cSD += 1u; bSD += b; }
-        }
+        if (valid) add_valid(cell, oow, dir, b);
+    }
+    // a record known to be valid: predicated adds, the rare out-of-window case as a branch
+    __device__ __forceinline__ void add_valid(uint32_t cell, bool oow, uint32_t dir, uint64_t b) {
+        const uint32_t s = cell >> 1, d = cell & 1u, sd = s & d;
+        cT += 1u; cS += s; cD += d; cSD += sd;
+        bT += b;
+        if (s) bS += b;
+        if (d) bD += b;
+        if (sd) bSD += b;
         if (oow) {
             if (dir == 0u) { oc[0] += 1u; ob[0] += b; } else { oc[1] += 1u; ob[1] += b; }
         }

@@ -38,12 +38,16 @@ __global__ void __launch_bounds__(256) k_map_keys(KernelParams p, uint32_t senti
         const uint64_t base = wbase + lane * 4ull;
         Rec4 r;
         load4(p, base, r);
+        uint32_t addr[8], in8[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { addr[2 * j] = r.src[j]; addr[2 * j + 1] = r.dst[j]; }
+        member_batch<8>(addr, in8, T);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool inrange = vvalid(p, base + j);
             const bool valid = inrange && watch_pass(r.src[j], r.dst[j], p);
-            const uint32_t s_in = member(r.src[j], T);
-            const uint32_t d_in = member(r.dst[j], T);
+            const uint32_t s_in = in8[2 * j];
+            const uint32_t d_in = in8[2 * j + 1];
             const uint32_t cell = s_in * 2u + d_in;
             const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
             uint32_t bin = 0;

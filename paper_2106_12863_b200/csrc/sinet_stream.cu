@@ -19,6 +19,8 @@
 // Records outside the window (late beyond the window, or a chunk wider than
 // it) take the same claim-then-RED path one at a time, so the result is exact
 // for any record order; only speed depends on time locality.
+#include <type_traits>
+
 #include "sinet_device.cuh"
 #include "sinet_kernels.h"
 
@@ -32,6 +34,21 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Predicated shared-memory updates of one (bin, dir) slot at shared address a (count word;
+// low bytes word at a + 8, high at a + 16): if take, count += 1 and low += lo, returning the
+// low word's old value (0 if not taken).
+__device__ __forceinline__ uint32_t smem_count_and_add_lo(uint32_t a, bool take, uint32_t lo) {
+    uint32_t old;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t"
+                 "@q red.shared.add.u32 [%1], 1;\n\t@q atom.shared.add.u32 %0, [%1+8], %3;\n\t}"
+                 : "=r"(old) : "r"(a), "r"((uint32_t)take), "r"(lo) : "memory");
+    return old;
+}
+__device__ __forceinline__ void smem_red_add_if(uint32_t a, bool take, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %2;\n\t}"
+                 ::"r"(a), "r"((uint32_t)take), "r"(v) : "memory");
 }
 
 // TMA bulk prefetch of [ptr, ptr + bytes) into L2 (16-byte aligned, multiple of 16; a hint)
@@ -307,6 +324,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (hi) atomicAdd(s + 4, hi);
     };
 
+    // Branch-free accumulate of RPT records: record j is added to its ring slot iff take[j]
+    // (predicated shared-memory RED / ATOM, no divergent branch).  The count and the high
+    // word use reductions without a return value; the low word an atomic whose old value
+    // gives the exact carry; all RPT low-word atomics are issued before any carry is needed.
+    const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(s_win);
+    auto accumulate_n = [&](const bool (&take)[RPT], const uint32_t (&bin)[RPT], const uint32_t (&dir)[RPT],
+                            const uint64_t (&by)[RPT]) {
+        uint32_t a[RPT], old[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            a[j] = win_base + ((bin[j] & (WS - 1)) * 6u + dir[j]) * 4u;
+            old[j] = smem_count_and_add_lo(a[j], take[j], (uint32_t)by[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const uint32_t lo = (uint32_t)by[j];
+            const uint32_t hi = (uint32_t)(by[j] >> 32) + ((old[j] + lo < old[j]) ? 1u : 0u);
+            smem_red_add_if(a[j] + 16u, take[j] && hi != 0u, hi);
+        }
+    };
+
     // Contiguous ranges of 4-record groups (virtual index space) are handed out
     // dynamically (one atomic per range, counter zeroed before each launch) so that
     // groups that finish early take more.
@@ -356,32 +394,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         WarpTotals ctot;   // this chunk's records (RPT == 2: reduced into shared memory below)
         if (kSmemTot) ctot.zero();
         WarpTotals& tt = kSmemTot ? ctot : tot;
+        uint32_t addr[2 * RPT], in8[2 * RPT];
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-            const bool valid = (full || (have && vvalid(p, my_v + j))) &&
-                               (!kWatch || watched(cur.src[j], p) || watched(cur.dst[j], p));
-            const uint32_t s_in = member(cur.src[j], T);
-            const uint32_t d_in = member(cur.dst[j], T);
-            const uint32_t cell = s_in * 2u + d_in;
-            const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
-            uint32_t bin = 0;
-            bool inw;
-            if (kW1) {   // 1 ms bins: the key is the offset itself
-                const uint64_t d = cur.ts[j] - p.start;
-                inw = d < (uint64_t)p.window;
-                bin = (uint32_t)d;
-            } else {
-                inw = map_bin(cur.ts[j], p, bin);
+        for (int j = 0; j < RPT; ++j) { addr[2 * j] = cur.src[j]; addr[2 * j + 1] = cur.dst[j]; }
+        member_batch<2 * RPT>(addr, in8, T);
+        bool inw4[RPT];
+        // kFull: every record of the chunk is valid (whole chunk in the batch, no watchlist),
+        // so the per-record validity tests and masks drop out of the common path
+        auto classify = [&](auto kFullTag) {
+            constexpr bool kAllValid = decltype(kFullTag)::value;
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const bool valid = kAllValid || ((full || (have && vvalid(p, my_v + j))) &&
+                                                 (!kWatch || watched(cur.src[j], p) || watched(cur.dst[j], p)));
+                const uint32_t cell = in8[2 * j] * 2u + in8[2 * j + 1];
+                const uint32_t dir = (p.lut >> (cell * 2u)) & 3u;
+                uint32_t bin = 0;
+                bool inw;
+                if (kW1) {   // 1 ms bins: the key is the offset itself
+                    const uint64_t d = cur.ts[j] - p.start;
+                    inw = d < (uint64_t)p.window;
+                    bin = (uint32_t)d;
+                } else {
+                    inw = map_bin(cur.ts[j], p, bin);
+                }
+                const bool directed = valid && dir < 2u;
+                binned4[j] = directed && inw;
+                bin4[j] = bin;
+                dir4[j] = dir;
+                inw4[j] = inw;
+                if (binned4[j]) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
+                if (kAllValid) tt.add_valid(cell, directed && !inw, dir, cur.by[j]);
+                else tt.add(valid, cell, directed && !inw, dir, cur.by[j]);
             }
-            const bool directed = valid && dir < 2u;
-            binned4[j] = directed && inw;
-            bin4[j] = bin;
-            dir4[j] = dir;
-            if (binned4[j]) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
-            if (tags_on) tag4 |= (s_in | (d_in << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
-            tt.add(valid, cell, directed && !inw, dir, cur.by[j]);
-        }
+        };
+        if (full && !kWatch) classify(std::true_type{});
+        else classify(std::false_type{});
         if (tags_on && have) {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j)
+                tag4 |= (in8[2 * j] | (in8[2 * j + 1] << 1) | ((inw4[j] ? 0u : 1u) << 2)) << (8 * j);
             if (RPT == 4) store_tags4(p, my_v, tag4);
             else for (int j = 0; j < RPT; ++j) if (vvalid(p, my_v + j)) p.tags[my_v + j - p.head] = (uint8_t)(tag4 >> (8 * j));
         }
@@ -412,10 +464,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (!kAgg && have_window) {
 #pragma unroll
             for (int j = 0; j < RPT; ++j)
-                if (binned4[j] && bin4[j] / kTileBins - act_t < lo_t + NT - act_t) {
-                    accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
-                    done4[j] = true;
-                }
+                done4[j] = binned4[j] && bin4[j] / kTileBins - act_t < lo_t + NT - act_t;
+            accumulate_n(done4, bin4, dir4, cur.by);
         }
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
@@ -459,9 +509,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         // the whole chunk inside the ring (the common case): no per-record residency/spill checks
         const bool all_in = any && bmin_t >= lo_t && bmax_t - lo_t < NT;
         if (!kAgg && all_in) {
+            bool rest[RPT];
+            bool any_rest = false;
 #pragma unroll
-            for (int j = 0; j < RPT; ++j)
-                if (binned4[j] && !done4[j]) accumulate(bin4[j], dir4[j], 1u, cur.by[j]);
+            for (int j = 0; j < RPT; ++j) { rest[j] = binned4[j] && !done4[j]; any_rest |= rest[j]; }
+            if (__any_sync(kFull, any_rest)) accumulate_n(rest, bin4, dir4, cur.by);
         } else
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {

@@ -307,3 +307,40 @@ def table_member_host(nets, lens, ips, labels=None) -> np.ndarray:
         ips.ctypes.data_as(ctypes.c_void_p), len(ips), out.ctypes.data_as(ctypes.c_void_p))
     check(rc, None, "table_member_host")
     return out
+
+
+def parse_text(text: torch.Tensor, tz_offset_min: int = 540, capacity: int | None = None,
+               status: bool = False, out: dict | None = None, workspace: torch.Tensor | None = None):
+    """NEXT-3: PA-7080 session-log text (uint8 CUDA tensor, Table 1 lines) -> device columns.
+
+    Marshals sinet_parse_text: returns (columns dict {ts, src, dst, bytes} of the valid lines
+    in line order, trimmed to the valid count; per-line status uint8 tensor or None;
+    the result counts as a dict).  Every step runs in libsinet.so.
+    """
+    assert text.is_cuda and text.dtype == torch.uint8 and text.is_contiguous()
+    n = text.numel()
+    dev = text.device
+    if capacity is None:
+        capacity = n // 62 + 1            # a valid line has >= 61 bytes + its newline
+    if out is None:
+        out = {"ts": torch.empty(capacity, dtype=torch.int64, device=dev),
+               "src": torch.empty(capacity, dtype=torch.int32, device=dev),
+               "dst": torch.empty(capacity, dtype=torch.int32, device=dev),
+               "bytes": torch.empty(capacity, dtype=torch.int64, device=dev)}
+    capacity = out["ts"].numel()
+    cols = N.Columns(_ptr(out["ts"]), _ptr(out["src"]), _ptr(out["dst"]), _ptr(out["bytes"]), capacity)
+    st = torch.empty(n + 1, dtype=torch.uint8, device=dev) if status else None
+    wsb = N.lib.sinet_parse_workspace_bytes(n)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    res = N.ParseResult()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = N.lib.sinet_parse_text(_ptr(text), n, tz_offset_min, ctypes.byref(cols), _ptr(st), st.numel() if st is not None else 0,
+                                _ptr(workspace), workspace.numel(), stream, ctypes.byref(res))
+    if rc != N.OK:
+        raise N.SinetError(rc, "parse_text: " + N.lib.sinet_parse_last_error().decode())
+    v = res.valid
+    cols_out = {k: t[:v] for k, t in out.items()}
+    info = {"lines": res.lines, "valid": v, "first_bad_line": res.first_bad_line,
+            "by_status": list(res.by_status)}
+    return cols_out, (st[:res.lines] if st is not None else None), info
