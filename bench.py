@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-comparator", action="store_true")
+    ap.add_argument("--no-parse", action="store_true", help="skip the NEXT-3 text-parse leg")
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
                     help="for ncu: no soak, no parity gate, no e2e, no CPU leg (numbers not valid)")
@@ -290,6 +291,11 @@ def run_ours(args):
     if not args.no_comparator and not args.profile and world == 1:
         comp = run_comparator(h, ts, src, dst, nb, args, wl)
 
+    # ---- NEXT-3: session-log text -> columns (the step before the path), rank 0 at N == 1
+    parse = None
+    if not args.no_parse and not args.profile and world == 1:
+        parse = run_parse_leg(S, wl, args, dev)
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e and not args.profile:
@@ -333,6 +339,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "comparator": comp,
+            "next3_parse": parse,
             "gpu_launches": launches,
             "clocks": clk,
             "parity_gate": gate,
@@ -434,6 +441,46 @@ def run_comparator(h, ts, src, dst, nb, args, wl):
     return {"impl": "paper design on B200: classify -> cub radix sort by (bin,dir) -> reduce_by_key + "
                     "run-length encode -> scatter (P:L213-214)", "ms_per_step": ms,
             "value": wl.n / (ms * 1e-3), "unit": UNIT, "bins_identical": same}
+
+
+def run_parse_leg(S, wl, args, dev, n_lines=5_000_000):
+    """NEXT-3 on this GPU: PA-7080 text (Table 1 lines, ~280 B each, synth/sinet_text.py) parsed
+    into the four columns by k_parse_text; checked against the generator's records, timed with
+    CUDA events.  Roofline bytes = text read once + 24 B per valid record written."""
+    import torch
+    from synth import records
+    from synth.sinet_text import session_text_batched
+    w = wl.with_(n=n_lines)
+    rec = records(w, 0, n_lines, device=dev)
+    text, _ = session_text_batched(w, rec)
+    del rec["cls"]
+    out = {"ts": torch.empty(n_lines, dtype=torch.int64, device=dev),
+           "src": torch.empty(n_lines, dtype=torch.int32, device=dev),
+           "dst": torch.empty(n_lines, dtype=torch.int32, device=dev),
+           "bytes": torch.empty(n_lines, dtype=torch.int64, device=dev)}
+    wsb = torch.empty(S._native.lib.sinet_parse_workspace_bytes(text.numel()), dtype=torch.uint8, device=dev)
+    k = max(3, min(args.steps, 10))
+    for _ in range(3):
+        cols, _, info = S.parse_text(text, 540, out=out, workspace=wsb)
+    ok = (info["valid"] == n_lines and all(torch.equal(cols[c], rec[c]) for c in ("ts", "src", "dst", "bytes")))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k):
+        S.parse_text(text, 540, out=out, workspace=wsb)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    nbytes = text.numel()
+    alg = nbytes + 24 * n_lines
+    bw = load_peaks().get("hbm_gbs", 6554.2)
+    res = {"lines": n_lines, "text_bytes": nbytes, "ms": ms, "records_per_s": n_lines / (ms * 1e-3),
+           "text_gbs": nbytes / (ms * 1e-3) / 1e9, "roofline_frac": alg / (ms * 1e-3) / 1e9 / bw,
+           "columns_equal_generator": bool(ok),
+           "note": "sinet_parse_text (k_parse_text), 5 M generated Table-1 lines, includes the result read-back sync"}
+    del text, out, wsb, rec
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_e2e(h, ts, src, dst, nb, args, world, local, barrier):

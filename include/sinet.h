@@ -335,9 +335,11 @@ int sinet_kernel_time(sinet_ctx* ctx, double* total_ms, uint64_t* launches);
 /* Which accumulation strategy the last classify call used (SINET_ORDER_STREAM/SHUFFLED, 3 = sort-reduce). */
 int sinet_last_strategy(const sinet_ctx* ctx);
 /* Host-side check of the prefix compiler (no GPU needed): compiles the CIDR
- * list exactly as sinet_open does and evaluates the same /16-class + boundary
- * lookup the kernels use, on the host, for ips[0..n): out[i] = member (0/1).
- * Errors: E_INVAL as sinet_open's table checks. */
+ * list exactly as sinet_open does and evaluates the lookups the kernels use
+ * (packed /16 classes + /24 level 2 + boundary search; the same without level
+ * 2; the byte /16 + /24 tables of the stream kernel) on the host, for
+ * ips[0..n): out[i] = member (0/1).
+ * Errors: E_INVAL as sinet_open's table checks, or if the encodings disagree. */
 int sinet_table_member_host(const uint32_t* prefix_net, const uint8_t* prefix_len, uint32_t n_prefixes,
                             const uint32_t* ips, uint64_t n, uint8_t* out);
 /* The same for a labelled table (sinet_open_labelled semantics). */
@@ -348,6 +350,15 @@ int sinet_table_member_host_labelled(const uint32_t* prefix_net, const uint8_t* 
  * stream_groups 0 = automatic, 1 = one 8192-bin ring per CTA, 2 = two independent
  * 4096-bin rings per CTA; warp_aggregation 1/0 = on/off, -1 = unchanged.  Errors: E_INVAL. */
 int sinet_set_tuning(sinet_ctx* ctx, int stream_groups, int warp_aggregation);
+/* Lookup-table encoding of the STREAM kernel (Alg. 1 l.6-9 compiled by sinet_open;
+ * results are identical for every setting): -1 = automatic (the fastest that fits
+ * in shared memory), 0 = byte /16 + /24 classes, 1 = packed 2-bit classes with
+ * level 2, 2 = packed without level 2, 3 = packed with level 2 and boundaries
+ * read from global memory.  A forced encoding that does not exist or fit falls
+ * back to the automatic choice.  Errors: E_INVAL (mode < -1 or > 3). */
+int sinet_set_table_mode(sinet_ctx* ctx, int mode);
+/* The encoding the next STREAM launch will use (0..3), or E_INVAL for a NULL ctx. */
+int sinet_table_mode(const sinet_ctx* ctx);
 /* Compile-time constants of this build. */
 uint32_t sinet_tile_bins(void);
 int sinet_abi_version(void);

@@ -96,6 +96,8 @@ _SIGS = {
     "sinet_kernel_time": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)], _i),
     "sinet_last_strategy": ([_vp], _i),
     "sinet_set_tuning": ([_vp, _i, _i], _i),
+    "sinet_set_table_mode": ([_vp, _i], _i),
+    "sinet_table_mode": ([_vp], _i),
     "sinet_watchlist_bytes": ([_u32], ctypes.c_size_t),
     "sinet_set_watchlist": ([_vp, _vp, _u32, _vp, ctypes.c_size_t], _i),
     "sinet_set_exchange": ([_vp, _i], _i),

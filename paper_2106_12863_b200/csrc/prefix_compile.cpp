@@ -167,6 +167,21 @@ bool compile_prefixes_labelled(const uint32_t* net, const uint8_t* len, const ui
         }
         ++m;
     }
+    out->b16.clear();
+    out->b24.clear();
+    if (out->n_mixed <= kMaxByteMixed) {
+        out->b16.assign(65536, 0u);
+        out->b24.assign((size_t)out->n_mixed * 256u, 0u);
+        uint32_t k = 0;
+        for (uint32_t x = 0; x < 65536; ++x) {
+            const uint32_t c = (out->cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
+            if (c != 2u) { out->b16[x] = (uint8_t)c; continue; }
+            out->b16[x] = (uint8_t)(2u + k);
+            for (uint32_t y = 0; y < 256; ++y)
+                out->b24[(size_t)k * 256u + y] = (uint8_t)((out->l2[(size_t)k * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u);
+            ++k;
+        }
+    }
     return true;
 }
 

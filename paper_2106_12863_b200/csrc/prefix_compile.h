@@ -28,12 +28,19 @@ struct CompiledTable {
     std::vector<uint32_t> rank;     // 2048 u32 = 4096 u16
     std::vector<uint32_t> mentry;
     std::vector<uint32_t> l2;
+    // byte encoding (only when n_mixed <= kMaxByteMixed), read by the stream kernel from
+    // shared memory with one byte load per level:
+    //   b16[x]         0 = block x out, 1 = in, 2 + m = mixed block number m
+    //   b24[m*256 + y] 0 / 1 / 2 (mixed -> search mentry[m]'s boundaries) for /24 y of block m
+    std::vector<uint8_t> b16;
+    std::vector<uint8_t> b24;
     uint32_t n_unique = 0;     // distinct normalised entries
     uint32_t n_intervals = 0;  // merged member intervals
     uint32_t n_mixed = 0;      // /16 blocks of class 2
 };
 
 constexpr uint32_t kMaxPrefixes = 16383;   // <= 4P+2 boundaries keeps lo and len in 16 bits each
+constexpr uint32_t kMaxByteMixed = 253;    // 2 + m fits a byte
 
 // Returns false (with *err set) on invalid input (n == 0, len > 32, n > kMaxPrefixes).
 bool compile_prefixes(const uint32_t* net, const uint8_t* len, uint32_t n,

@@ -98,7 +98,7 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, rank, mentry, l2, flags, sparse, counters, xranges, staging, staging_bytes, total;
+    size_t totals, cls2, entry, bnd, rank, mentry, l2, b16, b24, flags, sparse, counters, xranges, staging, staging_bytes, total;
 };
 
 // Device staging for the sparse multi-GPU exchange: a quarter of the owned slice, capped.
@@ -120,6 +120,8 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes, int world) {
     L.rank = off;   off = align_up(off + (size_t)kRankWords * 4, 256);
     L.mentry = off; off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 4, 256);
     L.l2 = off;     off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 64, 256);
+    L.b16 = off;    off = align_up(off + 65536, 256);
+    L.b24 = off;    off = align_up(off + (size_t)kMaxByteMixed * 256, 256);
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
     L.counters = off; off = align_up(off + 64, 256);   // [0] range counter, [4..5] touched min/max
@@ -156,6 +158,7 @@ struct sinet_ctx {
     uint32_t ranges_per_group = 0;
     uint32_t stream_threads = 0;
     uint32_t pf_chunks = 2;
+    int tab_mode = -1;            // stream kernel lookup-table encoding: -1 automatic, 0..3 forced
     int exchange = 0;             // multi-GPU merge: 0 auto (sparse when cheaper), 1 dense, 2 sparse
     int last_exchange = 0;        // 1 dense reduce-scatter, 2 sparse touched-range exchange
     // NEXT-2 watchlist (caller-owned device buffer)
@@ -218,6 +221,10 @@ KernelParams base_params(sinet_ctx* c) {
     p.rank = ws_u32(c, c->ws.rank);
     p.mentry = ws_u32(c, c->ws.mentry);
     p.l2 = ws_u32(c, c->ws.l2);
+    p.b16 = c->d_ws + c->ws.b16;
+    p.b24 = c->d_ws + c->ws.b24;
+    p.has_bytes = c->table.b16.empty() ? 0u : 1u;
+    p.tab_mode = c->tab_mode;
     p.n_mixed = c->table.n_mixed;
     p.nbnd = c->nbnd;
     p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
@@ -454,6 +461,7 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
     if (const char* t = std::getenv("SINET_STREAM_THREADS")) c->stream_threads = (uint32_t)std::atoi(t);
     if (const char* x = std::getenv("SINET_EXCHANGE")) c->exchange = std::atoi(x);
     if (const char* f = std::getenv("SINET_PF")) c->pf_chunks = (uint32_t)std::atoi(f);
+    if (const char* t = std::getenv("SINET_TAB")) c->tab_mode = std::atoi(t);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
@@ -467,6 +475,10 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.mentry, c->table.mentry.data(), c->table.mentry.size() * 4, cudaMemcpyHostToDevice, c->stream));
     if (!c->table.l2.empty())
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.l2, c->table.l2.data(), c->table.l2.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    if (!c->table.b16.empty())
+        OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.b16, c->table.b16.data(), 65536, cudaMemcpyHostToDevice, c->stream));
+    if (!c->table.b24.empty())
+        OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.b24, c->table.b24.data(), c->table.b24.size(), cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.counters, 0, 64, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.counters + 16, 0xFF, 4, c->stream));   // touched min = ~0
@@ -856,29 +868,47 @@ int sinet_table_member_host_labelled(const uint32_t* net, const uint8_t* len, co
     std::string err;
     if (!compile_prefixes_labelled(net, len, label, np, &t, &err)) return SINET_E_INVAL;
     if (n && (!ips || !out)) return SINET_E_INVAL;
-    for (uint64_t i = 0; i < n; ++i) {
-        // the kernels' lookup (sinet_device.cuh member()), evaluated on the host
-        uint32_t ip = ips[i], x = ip >> 16;
-        uint32_t c = (t.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
-        if (c < 2u) { out[i] = (uint8_t)c; continue; }
-        // mixed block: rank + level-2 /24 classes + per-block entry, exactly as the kernels'
-        // member() in sinet_device.cuh, with the dense per-/16 table as a cross-check
-        const uint32_t w = t.cls2[x >> 4], sh = (x & 15u) * 2u;
-        const uint32_t mixed = (w >> 1) & ~w & 0x55555555u;
-        const uint16_t* rk = reinterpret_cast<const uint16_t*>(t.rank.data());
-        const uint32_t mi = rk[x >> 4] + (uint32_t)__builtin_popcount(mixed & ((1u << sh) - 1u));
-        if (mi >= t.n_mixed || t.mentry[mi] != t.entry[x]) return SINET_E_INVAL;   // compiler bug
-        const uint32_t y = (ip >> 8) & 0xFFu;
-        const uint32_t c2 = (t.l2[(size_t)mi * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
-        if (c2 < 2u) { out[i] = (uint8_t)c2; continue; }
-        uint32_t e = t.mentry[mi], cnt = e & 0xFFFFu, m = e >> 16;
+    auto search = [&](uint32_t e, uint32_t ip) {   // #boundaries <= ip, from a block's entry
+        uint32_t cnt = e & 0xFFFFu, m = e >> 16;
         const uint32_t* b = t.bnd.data() + cnt;
         while (m) {
             uint32_t half = m >> 1;
             if (b[half] <= ip) { b += half + 1; cnt += half + 1; m -= half + 1; }
             else m = half;
         }
-        out[i] = (uint8_t)(cnt & 1u);
+        return cnt & 1u;
+    };
+    const bool have_bytes = !t.b16.empty();
+    for (uint64_t i = 0; i < n; ++i) {
+        // the kernels' lookups (sinet_device.cuh member() / member_batch(), all three table
+        // encodings), evaluated on the host; an encoding that disagrees is a compiler bug
+        uint32_t ip = ips[i], x = ip >> 16;
+        uint32_t c = (t.cls2[x >> 4] >> ((x & 15u) * 2u)) & 3u;
+        uint32_t r_packed = c, r_nol2 = c, r_byte = c;
+        if (c == 2u) {
+            // mixed block: rank + level-2 /24 classes + per-block entry
+            const uint32_t w = t.cls2[x >> 4], sh = (x & 15u) * 2u;
+            const uint32_t mixed = (w >> 1) & ~w & 0x55555555u;
+            const uint16_t* rk = reinterpret_cast<const uint16_t*>(t.rank.data());
+            const uint32_t mi = rk[x >> 4] + (uint32_t)__builtin_popcount(mixed & ((1u << sh) - 1u));
+            if (mi >= t.n_mixed || t.mentry[mi] != t.entry[x]) return SINET_E_INVAL;
+            const uint32_t y = (ip >> 8) & 0xFFu;
+            const uint32_t c2 = (t.l2[(size_t)mi * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
+            r_packed = (c2 < 2u) ? c2 : search(t.mentry[mi], ip);
+            r_nol2 = search(t.mentry[mi], ip);   // packed encoding without level 2
+        }
+        if (have_bytes) {   // byte encoding: b16, then b24 of the mixed block, then its search
+            const uint32_t b = t.b16[x];
+            if (b < 2u) r_byte = b;
+            else {
+                const uint32_t m = b - 2u, b2 = t.b24[(size_t)m * 256u + ((ip >> 8) & 0xFFu)];
+                r_byte = (b2 < 2u) ? b2 : search(t.mentry[m], ip);
+            }
+        } else {
+            r_byte = r_packed;
+        }
+        if (r_nol2 != r_packed || r_byte != r_packed) return SINET_E_INVAL;
+        out[i] = (uint8_t)r_packed;
     }
     return SINET_OK;
 }
@@ -894,6 +924,18 @@ int sinet_set_tuning(sinet_ctx* c, int stream_groups, int warp_aggregation) {
     c->stream_groups = (uint32_t)stream_groups;
     if (warp_aggregation >= 0) c->agg = warp_aggregation != 0;
     return SINET_OK;
+}
+
+int sinet_set_table_mode(sinet_ctx* c, int mode) {
+    if (!c) return SINET_E_INVAL;
+    if (mode < -1 || mode > 3) return fail(c, SINET_E_INVAL, "table mode must be -1 (automatic) or 0..3");
+    c->tab_mode = mode;
+    return SINET_OK;
+}
+
+int sinet_table_mode(const sinet_ctx* c) {
+    if (!c) return SINET_E_INVAL;
+    return stream_table_mode(!c->table.b16.empty(), c->nbnd, c->table.n_mixed, c->tab_mode);
 }
 
 int sinet_set_kernel_timing(sinet_ctx* c, int on) {

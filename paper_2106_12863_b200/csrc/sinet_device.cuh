@@ -90,6 +90,82 @@ __device__ __forceinline__ void member_batch(const uint32_t (&ip)[K], uint32_t (
     }
 }
 
+// #boundaries <= ip of a mixed block (its entry: first boundary | count << 16), odd = member
+__device__ __forceinline__ uint32_t block_search(uint32_t e, uint32_t ip, const uint32_t* bnd) {
+    uint32_t cnt = e & 0xFFFFu, len = e >> 16;
+    const uint32_t* b = bnd + cnt;
+    while (len) {
+        const uint32_t half = len >> 1;
+        if (b[half] <= ip) { b += half + 1; cnt += half + 1; len -= half + 1; }
+        else len = half;
+    }
+    return cnt & 1u;
+}
+
+// Byte encoding (stream kernel, kTabByte; prefix_compile.h): every level is one byte load.
+struct TableB {
+    const uint8_t* b16;      // smem [65536]: 0 out, 1 in, 2 + m mixed block m
+    const uint8_t* b24;      // smem [n_mixed * 256 (>= 16)]: 0 / 1 / 2 (mixed /24: search)
+    const uint32_t* mentry;  // smem
+    const uint32_t* bnd;     // smem
+};
+
+// member() of K addresses with the byte encoding: K byte loads of the /16 classes, then K
+// byte loads of the /24 classes (an address outside a mixed block loads b24[0] - the same
+// byte for every such lane, a broadcast - and keeps its class), branch-free; a mixed /24
+// (a prefix longer than /24) searches its block's boundaries.
+template <int K>
+__device__ __forceinline__ void member_batch_byte(const uint32_t (&ip)[K], uint32_t (&in)[K], const TableB& T) {
+    uint32_t c[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) c[k] = T.b16[ip[k] >> 16];
+    uint32_t m[K];
+    bool search = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const bool mixed = c[k] >= 2u;
+        m[k] = c[k] - 2u;
+        const uint32_t c2 = T.b24[mixed ? ((m[k] << 8) | ((ip[k] >> 8) & 0xFFu)) : 0u];
+        c[k] = mixed ? c2 : c[k];
+        search |= c[k] == 2u;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) in[k] = c[k] & 1u;
+    if (search) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (c[k] == 2u) in[k] = block_search(T.mentry[m[k]], ip[k], T.bnd);
+    }
+}
+
+// member() of K addresses with the packed encoding without level 2 (kTabPackedNoL2: large
+// lists whose level 2 does not fit in shared memory): a mixed /16 searches its boundaries.
+template <int K>
+__device__ __forceinline__ void member_batch_nol2(const uint32_t (&ip)[K], uint32_t (&in)[K], const Table& T) {
+    uint32_t w[K], r[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        w[k] = T.cls2[ip[k] >> 20];
+        r[k] = T.rank[ip[k] >> 20];
+    }
+    bool search = false;
+    uint32_t c[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t sh = ((ip[k] >> 16) & 15u) * 2u;
+        c[k] = (w[k] >> sh) & 3u;
+        const uint32_t mixed = (w[k] >> 1) & ~w[k] & 0x55555555u;
+        r[k] += __popc(mixed & ((1u << sh) - 1u));
+        in[k] = c[k] & 1u;
+        search |= c[k] == 2u;
+    }
+    if (search) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (c[k] == 2u) in[k] = block_search(T.mentry[r[k]], ip[k], T.bnd);
+    }
+}
+
 // ---------------------------------------------------------------- NEXT-2: watchlist predicate
 // Exact-address set (AbuseIPDB / GRIZZLY STEPPE lists): a /16 bitmap
 // rejects most addresses with one cached load, a binary search confirms the rest.
@@ -320,6 +396,53 @@ __device__ __forceinline__ Table stage_table(const KernelParams& p, uint32_t* sm
         T.bnd = p.bnd;
     }
     return T;
+}
+
+// Stream-kernel tables (kTab*, sinet_params.h), staged at `smem` (stream_table_bytes() bytes).
+template <int kTab> struct StreamTab { using T = Table; };
+template <> struct StreamTab<kTabByte> { using T = TableB; };
+
+template <int kTab>
+__device__ __forceinline__ typename StreamTab<kTab>::T stage_stream_table(const KernelParams& p, uint32_t* smem) {
+    if constexpr (kTab == kTabByte) {
+        TableB T;
+        uint4* s4 = reinterpret_cast<uint4*>(smem);
+        const uint4* g16 = reinterpret_cast<const uint4*>(p.b16);
+        for (uint32_t i = threadIdx.x; i < 65536u / 16u; i += blockDim.x) s4[i] = __ldg(g16 + i);
+        const uint32_t n24 = (p.n_mixed * 256u + 15u) / 16u + 1u;   // >= 16 bytes (b24[0] is always read)
+        uint4* s24 = s4 + 65536u / 16u;
+        const uint4* g24 = reinterpret_cast<const uint4*>(p.b24);
+        for (uint32_t i = threadIdx.x; i < n24; i += blockDim.x) s24[i] = __ldg(g24 + i);
+        uint32_t* s_me = reinterpret_cast<uint32_t*>(s24 + n24);
+        uint32_t* s_bnd = s_me + p.n_mixed;
+        for (uint32_t i = threadIdx.x; i < p.n_mixed; i += blockDim.x) s_me[i] = __ldg(p.mentry + i);
+        for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
+        T.b16 = reinterpret_cast<const uint8_t*>(s4);
+        T.b24 = reinterpret_cast<const uint8_t*>(s24);
+        T.mentry = s_me;
+        T.bnd = s_bnd;
+        return T;
+    } else if constexpr (kTab == kTabPackedNoL2) {
+        Table T = stage_table<false>(p, smem);
+        uint32_t* s_me = smem + kClsWords + kRankWords;
+        uint32_t* s_bnd = s_me + p.n_mixed;
+        for (uint32_t i = threadIdx.x; i < p.n_mixed; i += blockDim.x) s_me[i] = __ldg(p.mentry + i);
+        for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
+        T.l2 = nullptr;
+        T.mentry = s_me;
+        T.bnd = s_bnd;
+        return T;
+    } else {
+        return stage_table<kTab == kTabPacked>(p, smem);
+    }
+}
+
+template <int kTab, int K>
+__device__ __forceinline__ void member_batch_tab(const uint32_t (&ip)[K], uint32_t (&in)[K],
+                                                 const typename StreamTab<kTab>::T& T) {
+    if constexpr (kTab == kTabByte) member_batch_byte<K>(ip, in, T);
+    else if constexpr (kTab == kTabPackedNoL2) member_batch_nol2<K>(ip, in, T);
+    else member_batch<K>(ip, in, T);
 }
 
 }  // namespace sinet

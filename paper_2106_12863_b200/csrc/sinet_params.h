@@ -35,6 +35,10 @@ struct KernelParams {
     const uint32_t* rank;          // [2048] u16 pairs: mixed blocks before each class-table word
     const uint32_t* mentry;        // [n_mixed] entry of each mixed /16 block
     const uint32_t* l2;            // [n_mixed * 16] 2-bit /24 classes of the mixed /16 blocks
+    const uint8_t* b16;            // [65536] byte /16 classes (2 + m: mixed block m), if has_bytes
+    const uint8_t* b24;            // [n_mixed * 256] byte /24 classes of the mixed blocks
+    uint32_t has_bytes;            // 1: the byte encoding exists (n_mixed <= kMaxByteMixed)
+    int32_t tab_mode;              // stream kernel table encoding: -1 automatic, else forced (kTab*)
     uint32_t nbnd;
     uint32_t n_mixed;
     uint32_t small;                // 1: level 2, entries and boundaries fit in shared memory
@@ -68,5 +72,31 @@ inline unsigned long table_smem_bytes(uint32_t nbnd, uint32_t n_mixed, bool smal
     return (unsigned long)(kClsWords + kRankWords) * 4u + (small ? table_extra_bytes(nbnd, n_mixed) : 0u);
 }
 constexpr unsigned long kMaxTableSmem = (unsigned long)(kClsWords + kRankWords) * 4u + kSmallExtraBytes;
+
+// Lookup-table encodings of the stream kernel, all staged in shared memory except the last:
+//   BYTE       byte /16 classes (64 KB) + byte /24 classes of the mixed blocks + entries + boundaries
+//   PACKED     2-bit /16 classes + rank + 2-bit /24 level 2 + entries + boundaries
+//   PACKED_NOL2  the same without level 2 (a mixed /16 searches its boundaries)
+//   GLOBAL     2-bit /16 classes + rank in shared memory, the rest read from global memory
+enum : int { kTabByte = 0, kTabPacked = 1, kTabPackedNoL2 = 2, kTabGlobal = 3 };
+constexpr unsigned long kStreamTableSmem = 96ul * 1024ul;   // next to the 128 KB ring
+inline unsigned long stream_table_bytes(int mode, uint32_t nbnd, uint32_t n_mixed) {
+    const unsigned long tail = (unsigned long)n_mixed * 4u + (unsigned long)nbnd * 4u;   // entries + boundaries
+    switch (mode) {
+        case kTabByte: return 65536ul + (((unsigned long)n_mixed * 256u + 15u) & ~15ul) + 16u + tail;
+        case kTabPacked: return (unsigned long)(kClsWords + kRankWords) * 4u + (unsigned long)n_mixed * 64u + tail;
+        case kTabPackedNoL2: return (unsigned long)(kClsWords + kRankWords) * 4u + tail;
+        default: return (unsigned long)(kClsWords + kRankWords) * 4u;
+    }
+}
+// the fastest encoding that fits (forced: 0..3 if it fits, else the automatic choice)
+inline int stream_table_mode(bool has_bytes, uint32_t nbnd, uint32_t n_mixed, int forced = -1) {
+    auto fits = [&](int m) { return m == kTabGlobal || stream_table_bytes(m, nbnd, n_mixed) <= kStreamTableSmem; };
+    if (forced >= 0 && forced <= 3 && (forced != kTabByte || has_bytes) && fits(forced)) return forced;
+    if (has_bytes && fits(kTabByte)) return kTabByte;
+    if (fits(kTabPacked)) return kTabPacked;
+    if (fits(kTabPackedNoL2)) return kTabPackedNoL2;
+    return kTabGlobal;
+}
 
 }  // namespace sinet

@@ -37,7 +37,7 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 
 // Predicated shared-memory updates of one (bin, dir) slot at shared address a (count word;
-// low bytes word at a + 8, high at a + 16): if take, count += 1 and low += lo, returning the
+// low bytes word at a + 8): if take, count += 1 and low += lo, returning the
 // low word's old value (0 if not taken).
 __device__ __forceinline__ uint32_t smem_count_and_add_lo(uint32_t a, bool take, uint32_t lo) {
     uint32_t old;
@@ -45,10 +45,6 @@ __device__ __forceinline__ uint32_t smem_count_and_add_lo(uint32_t a, bool take,
                  "@q red.shared.add.u32 [%1], 1;\n\t@q atom.shared.add.u32 %0, [%1+8], %3;\n\t}"
                  : "=r"(old) : "r"(a), "r"((uint32_t)take), "r"(lo) : "memory");
     return old;
-}
-__device__ __forceinline__ void smem_red_add_if(uint32_t a, bool take, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %2;\n\t}"
-                 ::"r"(a), "r"((uint32_t)take), "r"(v) : "memory");
 }
 
 // TMA bulk prefetch of [ptr, ptr + bytes) into L2 (16-byte aligned, multiple of 16; a hint)
@@ -126,7 +122,7 @@ __device__ void spill_warp(const KernelParams& p, bool need, uint32_t bin, uint3
         const bool mine = need && t == tl;
         if (mine) {
             unsigned long long* slot = p.bins + ((size_t)bin * 4u + dir * 2u);
-            atomicAdd(slot, (unsigned long long)cnt);
+            if (cnt) atomicAdd(slot, (unsigned long long)cnt);
             if (bytes) atomicAdd(slot + 1, (unsigned long long)bytes);
         }
         pending &= ~__ballot_sync(kFull, mine);
@@ -155,16 +151,19 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
     }
 }
 
-// Shared-memory window: a ring of NT tiles x 256 ms bins, 6 u32 per bin =
-// {cnt_out, cnt_in, lo_out, lo_in, hi_out, hi_in} (array of structs: a thread retires one
-// bin as one full 32-byte sector, so a warp writes 1 KB contiguous per store pair).  Tiles [lo_t, lo_t + NT)
+// Shared-memory window: a ring of NT tiles x 256 ms bins, 4 u32 per bin =
+// {cnt_out, cnt_in, lo_out, lo_in}: the low 32 bits of the byte sums.  A record whose bytes
+// reach the high word (>= 2^32, or a carry out of the low word: elephants, very hot bins)
+// adds that part straight to HBM through the spill path, after the chunk barrier, when
+// the group holds no claim.  A thread retires one bin as one full 32-byte sector, so a
+// warp writes 1 KB contiguous per store pair.  Tiles [lo_t, lo_t + NT)
 // are resident.  After a chunk is accumulated, tiles below the chunk's
 // oldest bin (keeping >= NT/2-1 tiles of history) are claimed with one
 // non-blocking CAS each; the CAS resolves while the next chunk is loaded and
 // classified, and the tiles are retired (stored or added) right after.  A CTA
 // never waits on another CTA's tile while it holds an unreleased claim, so
 // the protocol cannot deadlock.
-template <int THREADS, int NG, int WS, int RPT, bool kAgg, bool kW1, bool kSmall, bool kWatch>
+template <int THREADS, int NG, int WS, int RPT, bool kAgg, bool kW1, int kTab, bool kWatch>
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // RPT records per thread per chunk; with RPT == 2 the side totals live in shared
     // memory per warp (registers for 1024 threads)
@@ -186,7 +185,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // NG independent groups per CTA, each with its own ring and half of the CTA's records;
     // the lookup table is shared.  A group synchronises on its own named barrier.
     const uint32_t gid = threadIdx.x / GT, tid = threadIdx.x % GT, lane = tid & 31u, warp = tid >> 5;
-    uint32_t* s_win = smem + gid * (WS * 6);
+    constexpr uint32_t kSlot = 4;             // u32 per ring bin
+    uint32_t* s_win = smem + gid * (WS * kSlot);
     uint32_t (*s_red)[2][GW] = s_red_all[gid];
     uint32_t* s_state = s_state_all[gid];
     auto group_sync = [&]() {
@@ -194,10 +194,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         else asm volatile("bar.sync %0, %1;" ::"r"(1u + gid), "r"((uint32_t)GT) : "memory");
     };
     const uint32_t prev_word = p.epoch > 1 ? (((p.epoch - 1u) << 2) | kTileInit) : 0u;
-    for (uint32_t i = threadIdx.x; i < (uint32_t)NG * WS * 6u / 4u; i += THREADS)
+    for (uint32_t i = threadIdx.x; i < (uint32_t)NG * WS * kSlot / 4u; i += THREADS)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (threadIdx.x < NG * NT) s_state_all[threadIdx.x / NT][threadIdx.x % NT] = 0u;
-    const Table T = stage_table<kSmall>(p, smem + NG * WS * 6);
+    const auto T = stage_stream_table<kTab>(p, smem + NG * WS * kSlot);
     __syncthreads();
 
     uint32_t lo_t = 0, act_t = 0;   // resident tiles [lo_t, lo_t+NT); [lo_t, act_t) claimed, to retire
@@ -229,23 +229,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // write (won: plain stores) or add (RED) 4 consecutive bins of the ring to HBM and zero them
     // write (won: plain stores) or add (RED) one bin of the ring to HBM and zero it
     auto flush_bin = [&](uint32_t bin, bool won) {
-        uint32_t* s = s_win + (bin & (WS - 1)) * 6u;
-        const uint2 c = *reinterpret_cast<const uint2*>(s);
-        const uint2 lo = *reinterpret_cast<const uint2*>(s + 2);
-        const uint2 hi = *reinterpret_cast<const uint2*>(s + 4);
-        *reinterpret_cast<uint2*>(s) = make_uint2(0u, 0u);
-        *reinterpret_cast<uint2*>(s + 2) = make_uint2(0u, 0u);
-        *reinterpret_cast<uint2*>(s + 4) = make_uint2(0u, 0u);
-        const unsigned long long b_out = (unsigned long long)lo.x | ((unsigned long long)hi.x << 32);
-        const unsigned long long b_in = (unsigned long long)lo.y | ((unsigned long long)hi.y << 32);
+        uint4* s = reinterpret_cast<uint4*>(s_win + (bin & (WS - 1)) * kSlot);
+        const uint4 v = *s;   // {cnt_out, cnt_in, lo_out, lo_in}
+        *s = make_uint4(0u, 0u, 0u, 0u);
         unsigned long long* g64 = p.bins + (size_t)bin * 4u;
         if (won) {
             ulonglong2* g = reinterpret_cast<ulonglong2*>(g64);
-            __stcg(g, make_ulonglong2(c.x, b_out));
-            __stcg(g + 1, make_ulonglong2(c.y, b_in));
+            __stcg(g, make_ulonglong2(v.x, v.z));
+            __stcg(g + 1, make_ulonglong2(v.y, v.w));
         } else {
-            if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (b_out) atomicAdd(g64 + 1, b_out); }
-            if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y); if (b_in) atomicAdd(g64 + 3, b_in); }
+            // a record with bytes but no count never reaches the ring (counts are >= 1)
+            if (v.x) { atomicAdd(g64, (unsigned long long)v.x); if (v.z) atomicAdd(g64 + 1, (unsigned long long)v.z); }
+            if (v.y) { atomicAdd(g64 + 2, (unsigned long long)v.y); if (v.w) atomicAdd(g64 + 3, (unsigned long long)v.w); }
         }
     };
 
@@ -313,35 +308,35 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         }
     };
 
-    // accumulate (cnt, bytes) of one (bin, dir) into the ring (caller checked residency)
-    auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) {
-        uint32_t* s = s_win + (bin & (WS - 1)) * 6u + dir;
+    // accumulate (cnt, bytes) of one (bin, dir) into the ring (caller checked residency);
+    // returns the high word (bytes >> 32 + the carry out of the low word, mod 2^32) that the
+    // caller must add to HBM as hi << 32 (exact mod 2^64)
+    auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) -> uint32_t {
+        uint32_t* s = s_win + (bin & (WS - 1)) * kSlot + dir;
         atomicAdd(s, cnt);
         const uint32_t lo = (uint32_t)bytes;
-        uint32_t hi = (uint32_t)(bytes >> 32);
         const uint32_t old = atomicAdd(s + 2, lo);
-        hi += (old + lo < old) ? 1u : 0u;     // exact carry out of the low word
-        if (hi) atomicAdd(s + 4, hi);
+        return (uint32_t)(bytes >> 32) + ((old + lo < old) ? 1u : 0u);
     };
 
     // Branch-free accumulate of RPT records: record j is added to its ring slot iff take[j]
-    // (predicated shared-memory RED / ATOM, no divergent branch).  The count and the high
-    // word use reductions without a return value; the low word an atomic whose old value
-    // gives the exact carry; all RPT low-word atomics are issued before any carry is needed.
+    // (predicated shared-memory RED / ATOM, no divergent branch).  The count uses a reduction
+    // without a return value, the low word an atomic whose old value gives the exact carry.
+    // Adds each taken record's high word (see accumulate) to hi[j].
     const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(s_win);
     auto accumulate_n = [&](const bool (&take)[RPT], const uint32_t (&bin)[RPT], const uint32_t (&dir)[RPT],
-                            const uint64_t (&by)[RPT]) {
-        uint32_t a[RPT], old[RPT];
+                            const uint64_t (&by)[RPT], uint32_t (&hi)[RPT]) {
+        uint32_t old[RPT];
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            a[j] = win_base + ((bin[j] & (WS - 1)) * 6u + dir[j]) * 4u;
-            old[j] = smem_count_and_add_lo(a[j], take[j], (uint32_t)by[j]);
+            const uint32_t a = win_base + ((bin[j] & (WS - 1)) * kSlot + dir[j]) * 4u;
+            old[j] = smem_count_and_add_lo(a, take[j], (uint32_t)by[j]);
         }
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const uint32_t lo = (uint32_t)by[j];
-            const uint32_t hi = (uint32_t)(by[j] >> 32) + ((old[j] + lo < old[j]) ? 1u : 0u);
-            smem_red_add_if(a[j] + 16u, take[j] && hi != 0u, hi);
+            const uint32_t h = (uint32_t)(by[j] >> 32) + ((old[j] + lo < old[j]) ? 1u : 0u);
+            hi[j] += take[j] ? h : 0u;
         }
     };
 
@@ -397,7 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         uint32_t addr[2 * RPT], in8[2 * RPT];
 #pragma unroll
         for (int j = 0; j < RPT; ++j) { addr[2 * j] = cur.src[j]; addr[2 * j + 1] = cur.dst[j]; }
-        member_batch<2 * RPT>(addr, in8, T);
+        member_batch_tab<kTab, 2 * RPT>(addr, in8, T);
         bool inw4[RPT];
         // kFull: every record of the chunk is valid (whole chunk in the batch, no watchlist),
         // so the per-record validity tests and masks drop out of the common path
@@ -459,13 +454,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         // (>= lo_t + NT): retire only touches the slots of [lo_t, act_t).  Warps do this work
         // instead of waiting at the barrier; the rest is accumulated after the retire.
         bool done4[RPT];
+        uint32_t hi4[RPT];   // high words owed to HBM (added after the barrier)
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) done4[j] = false;
+        for (int j = 0; j < RPT; ++j) { done4[j] = false; hi4[j] = 0u; }
         if (!kAgg && have_window) {
 #pragma unroll
             for (int j = 0; j < RPT; ++j)
                 done4[j] = binned4[j] && bin4[j] / kTileBins - act_t < lo_t + NT - act_t;
-            accumulate_n(done4, bin4, dir4, cur.by);
+            accumulate_n(done4, bin4, dir4, cur.by, hi4);
         }
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
@@ -513,7 +509,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             bool any_rest = false;
 #pragma unroll
             for (int j = 0; j < RPT; ++j) { rest[j] = binned4[j] && !done4[j]; any_rest |= rest[j]; }
-            if (__any_sync(kFull, any_rest)) accumulate_n(rest, bin4, dir4, cur.by);
+            if (__any_sync(kFull, any_rest)) accumulate_n(rest, bin4, dir4, cur.by, hi4);
+            bool any_hi = false;
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) any_hi |= hi4[j] != 0u;
+            if (__any_sync(kFull, any_hi)) {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (__any_sync(kFull, hi4[j] != 0u))
+                        spill_warp(p, hi4[j] != 0u, bin4[j], dir4[j], 0u, (uint64_t)hi4[j] << 32);
+            }
         } else
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
@@ -554,8 +559,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                 }
             }
             const bool in_ring = act && (bin4[j] / kTileBins - lo_t < NT);
-            if (in_ring) accumulate(bin4[j], dir4[j], cnt, byt);
-            if (__any_sync(kFull, act && !in_ring)) spill_warp(p, act && !in_ring, bin4[j], dir4[j], cnt, byt);
+            // high word owed by this record (accumulated now, or before the barrier)
+            const uint32_t hv = hi4[j] + (in_ring ? accumulate(bin4[j], dir4[j], cnt, byt) : 0u);
+            const bool out = act && !in_ring;
+            if (__any_sync(kFull, out || hv != 0u))
+                spill_warp(p, out || hv != 0u, bin4[j], dir4[j], out ? cnt : 0u, out ? byt : ((uint64_t)hv << 32));
         }
         cur = nxt;
 
@@ -604,16 +612,18 @@ constexpr int kRingBins2 = 4096;
 // (The kernel also supports 1024 threads x 2 records, measured 23 % slower: not instantiated.)
 #define SINET_STREAM_KERNEL(G, A, W, S, WL) \
     k_hist_stream<512, G, (G == 1 ? kRingBins1 : kRingBins2), 4, A, W, S, WL>
+constexpr size_t kRingSmem = (size_t)kRingBins1 * 4u * 4u;   // 128 KB: 4 u32 per bin
 
 cudaError_t setup_hist_stream() {
-    const int mx = (int)((size_t)kRingBins1 * 6u * 4u + kMaxTableSmem);
+    const int mx = (int)(kRingSmem + kStreamTableSmem);
     cudaError_t e;
 #define SET(G, A, W, S, WL)                                                                                 \
     e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W, S, WL), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
 #define SET4(G, S, WL) SET(G, true, true, S, WL) SET(G, true, false, S, WL) SET(G, false, true, S, WL) SET(G, false, false, S, WL)
-    SET4(1, true, false) SET4(1, false, false) SET4(2, true, false) SET4(2, false, false)
-    SET4(1, true, true) SET4(1, false, true) SET4(2, true, true) SET4(2, false, true)
+#define SETT(G, WL) SET4(G, kTabByte, WL) SET4(G, kTabPacked, WL) SET4(G, kTabPackedNoL2, WL) SET4(G, kTabGlobal, WL)
+    SETT(1, false) SETT(2, false) SETT(1, true) SETT(2, true)
+#undef SETT
 #undef SET4
 #undef SET
     return cudaSuccess;
@@ -627,7 +637,8 @@ int stream_groups_for(const KernelParams& p) {
 
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st) {
     static_assert(kRingBins1 == 2 * kRingBins2, "both layouts use the same shared memory");
-    const size_t sm = (size_t)kRingBins1 * 6u * 4u + table_smem_bytes(p.nbnd, p.n_mixed, p.small);
+    const int tab = stream_table_mode(p.has_bytes != 0u, p.nbnd, p.n_mixed, p.tab_mode);
+    const size_t sm = kRingSmem + stream_table_bytes(tab, p.nbnd, p.n_mixed);
     const uint64_t chunks = (p.nv / 4 + 511) / 512;
     const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
     const bool w1 = p.width == 1u;
@@ -644,8 +655,14 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     else if (w1) SINET_STREAM_KERNEL(G, false, true, S, WL)<<<grid, 512, sm, st>>>(q);                   \
     else SINET_STREAM_KERNEL(G, false, false, S, WL)<<<grid, 512, sm, st>>>(q);
 #define LAUNCH_G(S, WL) if (g == 2) { LAUNCH(2, S, WL) } else { LAUNCH(1, S, WL) }
-    if (p.wn) { if (p.small) { LAUNCH_G(true, true) } else { LAUNCH_G(false, true) } }
-    else { if (p.small) { LAUNCH_G(true, false) } else { LAUNCH_G(false, false) } }
+#define LAUNCH_T(WL) switch (tab) {                              \
+        case kTabByte: LAUNCH_G(kTabByte, WL) break;                  \
+        case kTabPacked: LAUNCH_G(kTabPacked, WL) break;              \
+        case kTabPackedNoL2: LAUNCH_G(kTabPackedNoL2, WL) break;      \
+        default: LAUNCH_G(kTabGlobal, WL) break;                      \
+    }
+    if (p.wn) { LAUNCH_T(true) } else { LAUNCH_T(false) }
+#undef LAUNCH_T
 #undef LAUNCH_G
 #undef LAUNCH
     return cudaGetLastError();

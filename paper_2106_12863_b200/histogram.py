@@ -274,6 +274,14 @@ class SinetHistogram:
         """Stream-kernel layout (0 auto / 1 / 2 groups) and warp aggregation (1/0, -1 unchanged)."""
         check(lib.sinet_set_tuning(self.ctx, stream_groups, warp_aggregation), self.ctx, "set_tuning")
 
+    def set_table_mode(self, mode: int = -1):
+        """Stream-kernel lookup-table encoding: -1 auto, 0 byte, 1 packed, 2 packed w/o level 2, 3 global."""
+        check(lib.sinet_set_table_mode(self.ctx, mode), self.ctx, "set_table_mode")
+
+    @property
+    def table_mode(self) -> int:
+        return int(lib.sinet_table_mode(self.ctx))
+
     def set_kernel_timing(self, on: bool):
         check(lib.sinet_set_kernel_timing(self.ctx, 1 if on else 0), self.ctx, "timing")
 

@@ -34,9 +34,10 @@ def dev_cols(cols, device="cuda"):
 
 
 def gpu_run(S, nets, lens, cols, start, window, width=1, lut=LUT_SRC_PRIORITY, order=0, chunks=None,
-            tags=False, groups=0, agg=-1):
+            tags=False, groups=0, agg=-1, tab=-1):
     h = S.SinetHistogram(nets, lens, start, window, width, lut=lut, order=order)
     h.set_tuning(groups, agg)
+    h.set_table_mode(tab)
     d = dev_cols(cols)
     n = d[0].numel()
     tg = torch.full((max(n, 4),), 0xEE, dtype=torch.uint8, device="cuda") if tags else None
@@ -98,6 +99,30 @@ def test_adversarial_parity(S, oracle_lib, lut, width, order, groups):
         assert_parity(g, o)
         np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
                                                                  start, window))
+
+
+@pytest.mark.parametrize("table", ["c1", "c5", "c5_first100"])
+@pytest.mark.parametrize("tab", [0, 1, 2, 3])
+def test_table_encodings_parity(S, oracle_lib, table, tab):
+    """Every lookup-table encoding of the stream kernel (byte, packed, packed without level 2,
+    global), on a SINET-like list, the 4096-entry /8-/32 list and a byte-sized /8-/32 list with
+    prefixes longer than /24; records hit every interval edge +-1 and carry > 2^32 bytes (the
+    ring's high-word spill).  An encoding that does not fit falls back to the automatic one."""
+    nets, lens = prefix_table(WORKLOADS[table.split("_")[0]])
+    if table.endswith("first100"):
+        nets, lens = nets[:100], lens[:100]
+    start, window = 1_613_660_400_000, 2_000_000
+    for n in (129, 60_001):
+        cols = _adversarial(n, nets, lens, start, window, seed=n + tab)
+        cols = (np.sort(cols[0]),) + cols[1:]     # time ordered: the stream kernel's ring path
+        for groups in (1, 2):
+            g = gpu_run(S, nets, lens, cols, start, window, order=1, tags=True, groups=groups, tab=tab)
+            o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, 1)
+            assert_parity(g, o)
+            np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
+                                                                     start, window))
+    # c5: no byte encoding (> 253 mixed /16 blocks) and its level 2 does not fit next to the ring
+    assert g["h"].table_mode == (2 if table == "c5" and tab in (0, 1) else tab)
 
 
 @pytest.mark.parametrize("wl_name,order", [("c1", "stream"), ("c1", "shuffled")])

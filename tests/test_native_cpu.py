@@ -71,10 +71,14 @@ def test_invalid_table_rejected():
         table_member_host([1], [40], [5])
 
 
-@pytest.mark.parametrize("wl", ["c1", "c2", "c5"])
+@pytest.mark.parametrize("wl", ["c1", "c2", "c5", "c5_first100"])
 def test_compiled_table_matches_oracle(oracle_lib, wl):
-    """Prefix compiler (a1) + the kernels' lookup == the oracle's literal linear scan."""
-    nets, lens = prefix_table(WORKLOADS[wl])
+    """Prefix compiler (a1) + the kernels' lookups (every table encoding, checked against each
+    other inside table_member_host) == the oracle's literal linear scan.  c5_first100: a
+    /8-/32 list small enough for the byte encoding, with prefixes longer than /24."""
+    nets, lens = prefix_table(WORKLOADS[wl.split("_")[0]])
+    if wl.endswith("first100"):
+        nets, lens = nets[:100], lens[:100]
     rng = np.random.default_rng(5)
     edges = edge_addresses(nets, lens)
     ips = np.concatenate([edges, rng.integers(0, 1 << 32, 20_000 if wl == "c5" else 200_000,
