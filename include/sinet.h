@@ -361,6 +361,7 @@ int sinet_set_table_mode(sinet_ctx* ctx, int mode);
 int sinet_table_mode(const sinet_ctx* ctx);
 /* Compile-time constants of this build. */
 uint32_t sinet_tile_bins(void);
+uint32_t sinet_parse_chunk_bytes(void);   /* text bytes one CTA of sinet_parse_text owns per ticket */
 int sinet_abi_version(void);
 
 #ifdef __cplusplus

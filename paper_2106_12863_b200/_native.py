@@ -70,6 +70,7 @@ _CP = ctypes.POINTER(Config)
 _SIGS = {
     "sinet_abi_version": ([], _i),
     "sinet_tile_bins": ([], _u32),
+    "sinet_parse_chunk_bytes": ([], _u32),
     "sinet_bins_bytes": ([_CP], ctypes.c_size_t),
     "sinet_workspace_bytes": ([_CP, _u32], ctypes.c_size_t),
     "sinet_staging_bytes": ([_u64], ctypes.c_size_t),

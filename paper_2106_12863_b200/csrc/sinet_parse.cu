@@ -8,16 +8,19 @@
 // dotted-quad IPv4 ("translated to a 32-bit sequence"), bytes a
 // decimal u64; per-line status, valid lines written in line order.
 //
-// B200 design: one pass over the text in HBM.  Persistent CTAs take 48 KB chunks
-// by ticket; each chunk (+ a 2 KB tail for the line that crosses its end) is
-// staged into shared memory by a TMA bulk copy (cp.async.bulk, mbarrier
+// B200 design: one pass over the text in HBM.  Persistent CTAs (several per SM) take
+// 16 KB chunks by ticket; each chunk (+ a 2 KB tail for the line that crosses its
+// end) is staged into shared memory by a TMA bulk copy (cp.async.bulk, mbarrier
 // completion), double buffered so the next chunk streams in while this one is
 // parsed.  A chunk owns the lines that start right after one of its newlines
-// (chunk 0 also the line at offset 0).  The CTA counts them (block scan), one
-// thread parses one line from shared memory, and the chunk's (lines, valid)
-// counts go through a decoupled look-back (two chained scans) that gives the
-// line index and the output index of its first line, so valid records are
-// compacted in line order without a second pass over the text.
+// (chunk 0 also the line at offset 0).  Every thread first turns 32-byte words of
+// the staged text into newline and comma bitmasks (structural index, 1 bit per
+// byte); the CTA counts line starts (block scan); one thread per line then finds
+// the line end and the commas around fields 1, 5, 8 and 21 with popcounts over the
+// bitmask words and parses those four fields; the chunk's (lines, valid) counts go
+// through a decoupled look-back (two chained scans) that gives the line index and
+// the output index of its first line, so valid records are compacted in line order
+// without a second pass over the text.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -26,17 +29,19 @@
 namespace sinet {
 namespace {
 
-constexpr int kPT = 256;                       // threads per CTA
+constexpr int kPT = 128;                       // threads per CTA
 constexpr uint32_t kChunk = kParseChunk;       // bytes owned per chunk
 constexpr uint32_t kTail = 2048;               // staged beyond the chunk: max line 2047 + '\n'
 constexpr uint32_t kBuf = kChunk + kTail;      // staged bytes per buffer
 constexpr uint32_t kBufAlloc = kBuf + 16;      // + slack: the word loop may read 3 bytes past the text
-constexpr int kLPT = 2;                        // lines per thread per round
+constexpr int kLPT = 1;                        // lines per thread per round
 constexpr uint32_t kLCap = kPT * kLPT;         // lines per round
 constexpr uint32_t kMaxLine = 2047;
 constexpr uint32_t kNoLine = 0xFFu;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+constexpr uint32_t kWords = kBuf / 32u;        // bitmask words of a staged buffer (1 bit per byte)
 static_assert(kChunk % (16 * kPT) == 0, "each thread scans a whole number of 16-byte words");
+static_assert(kBuf % 32u == 0, "whole bitmask words");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -158,42 +163,70 @@ struct LineOut {
     uint32_t src, dst, status;
 };
 
-// Parse the line starting at buf[s] (chunk-local); lim = bytes of text staged from
-// s on that belong to the text (<= kMaxLine + 1 is enough to decide).
-__device__ LineOut parse_line(const uint8_t* buf, uint32_t s, uint32_t lim, int64_t tz_ms) {
+// 4-bit mask of the bytes of w equal to the byte pattern pat (bit i = byte i): exact
+// per-byte zero test of w ^ pat, flags gathered by one multiply.
+__device__ __forceinline__ uint32_t eq_nibble(uint32_t w, uint32_t pat) {
+    const uint32_t x = w ^ pat;
+    const uint32_t f = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;   // bit 7 of each zero byte
+    return ((f >> 7) * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t eq_mask32(const uint4& v0, const uint4& v1, uint32_t pat) {
+    return eq_nibble(v0.x, pat) | (eq_nibble(v0.y, pat) << 4) | (eq_nibble(v0.z, pat) << 8) |
+           (eq_nibble(v0.w, pat) << 12) | (eq_nibble(v1.x, pat) << 16) | (eq_nibble(v1.y, pat) << 20) |
+           (eq_nibble(v1.z, pat) << 24) | (eq_nibble(v1.w, pat) << 28);
+}
+
+// position of the n-th (0-based) set bit of m (n < popc(m))
+__device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t n) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (uint32_t w = 16; w >= 1; w >>= 1) {
+        const uint32_t c = __popc(m & ((1u << w) - 1u));
+        if (n >= c) { n -= c; m >>= w; pos += w; }
+    }
+    return pos;
+}
+
+// Parse the line starting at buf[s] (chunk-local), with the chunk's newline / comma bitmask
+// words nlm / cmm; lim = bytes of text staged from s on (<= kMaxLine + 1 is enough to decide).
+__device__ LineOut parse_line(const uint8_t* buf, const uint32_t* nlm, const uint32_t* cmm, uint32_t s,
+                              uint32_t lim, int64_t tz_ms) {
     LineOut o;
     o.ts = 0; o.bytes = 0; o.src = 0; o.dst = 0;
-    // scan for the end and the commas that bound fields 1, 5, 8 and 21 (0-based 0, 4, 7, 20)
-    uint32_t nc = 0, c0 = 0, c3 = 0, c4 = 0, c6 = 0, c7 = 0, c19 = 0, c20 = 0;
+    // the end and the commas that bound fields 1, 5, 8 and 21 (comma ordinals 0, 3-4, 6-7, 19-20)
+    // the ordinals 0, 3, 4, 6, 7, 19, 20 packed as 5-bit fields (no indexed local array)
+    constexpr uint64_t kT = 0ull | 3ull << 5 | 4ull << 10 | 6ull << 15 | 7ull << 20 | 19ull << 25 | 20ull << 30;
+    auto target = [&](uint32_t i) { return (uint32_t)(kT >> (5u * i)) & 31u; };
+    uint32_t nc = 0, ti = 0, c0 = 0, c3 = 0, c4 = 0, c6 = 0, c7 = 0, c19 = 0, c20 = 0;
     uint32_t e = 0xFFFFFFFFu;                         // offset of '\n' from s
     const uint32_t stop = min(lim, kMaxLine + 1u);
-    uint32_t w0 = s & ~3u;                            // aligned word loop over [s, s + stop)
-    for (uint32_t a = w0; a < s + stop && e == 0xFFFFFFFFu; a += 4u) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(buf + a);
+    for (uint32_t wi = s >> 5; wi * 32u < s + stop; ++wi) {
+        const uint32_t base = wi * 32u;
         uint32_t valid = 0xFFFFFFFFu;
-        if (a < s) valid <<= 8u * (s - a);            // bytes before the line start
-        const uint32_t rem = s + stop - a;
-        if (rem < 4u) valid &= (1u << (8u * rem)) - 1u;
-        const uint32_t nl = __vcmpeq4(w, 0x0A0A0A0Au) & valid;
-        uint32_t cm = __vcmpeq4(w, 0x2C2C2C2Cu) & valid;
+        if (base < s) valid <<= (s - base);           // bytes before the line start
+        const uint32_t rem = s + stop - base;
+        if (rem < 32u) valid &= (1u << rem) - 1u;
+        const uint32_t nl = nlm[wi] & valid;
+        uint32_t cm = cmm[wi] & valid;
         if (nl) {
-            const uint32_t bpos = (__ffs(nl) - 1u) >> 3;
-            e = a + bpos - s;
-            cm &= (1u << (8u * bpos)) - 1u;            // commas before the newline only
+            const uint32_t bp = __ffs(nl) - 1u;
+            e = base + bp - s;
+            cm &= (1u << bp) - 1u;                     // commas before the newline only
         }
-        while (cm) {
-            const uint32_t bpos = (__ffs(cm) - 1u) >> 3;
-            cm &= ~(0xFFu << (8u * bpos));
-            const uint32_t q = a + bpos;
-            if (nc == 0u) c0 = q;
-            if (nc == 3u) c3 = q;
-            if (nc == 4u) c4 = q;
-            if (nc == 6u) c6 = q;
-            if (nc == 7u) c7 = q;
-            if (nc == 19u) c19 = q;
-            if (nc == 20u) c20 = q;
-            ++nc;
+        const uint32_t c = __popc(cm);
+        while (ti < 7u && target(ti) < nc + c) {
+            const uint32_t q = base + nth_bit(cm, target(ti) - nc);
+            c0 = ti == 0u ? q : c0;
+            c3 = ti == 1u ? q : c3;
+            c4 = ti == 2u ? q : c4;
+            c6 = ti == 3u ? q : c6;
+            c7 = ti == 4u ? q : c7;
+            c19 = ti == 5u ? q : c19;
+            c20 = ti == 6u ? q : c20;
+            ++ti;
         }
+        nc += c;
+        if (e != 0xFFFFFFFFu) break;
     }
     uint32_t len = (e == 0xFFFFFFFFu) ? stop : e;   // content length (no '\n')
     if (len > kMaxLine) { o.status = kLineLong; return o; }
@@ -230,16 +263,19 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* s_w, uint32
     return base + x - v;
 }
 
-// Decoupled look-back over one chained scan: publishes this chunk's aggregate, returns
-// the exclusive prefix (sum of all earlier chunks) and publishes the inclusive value.
-// Called by warp 0; lane k inspects predecessor chunk (c - 1 - k) of each window.
-__device__ uint64_t look_back(unsigned long long* st, uint64_t c, uint64_t agg) {
+// Decoupled look-back over one chained scan, in two steps so that a CTA can publish a
+// chunk's aggregate as soon as it is parsed and look back later (after parsing its next
+// chunk), when the predecessors have published theirs.
+// publish_agg: thread 0; chunk 0 publishes its inclusive value at once.
+__device__ __forceinline__ void publish_agg(unsigned long long* st, uint64_t c, uint64_t agg) {
+    st_release_u64(st + c, (c == 0 ? kFlagInc : kFlagAgg) | agg);
+}
+// finish_look_back: warp 0; returns the exclusive prefix of chunk c (the sum over all
+// earlier chunks) and publishes its inclusive value.  Lane k inspects predecessor
+// (c - 1 - k) of each window of 32.
+__device__ uint64_t finish_look_back(unsigned long long* st, uint64_t c, uint64_t agg) {
     const uint32_t lane = threadIdx.x & 31u;
-    if (c == 0) {
-        if (lane == 0) st_release_u64(st, kFlagInc | agg);
-        return 0;
-    }
-    if (lane == 0) st_release_u64(st + c, kFlagAgg | agg);
+    if (c == 0) return 0;
     uint64_t excl = 0;
     int64_t j = (int64_t)c - 1;
     for (;;) {
@@ -247,7 +283,10 @@ __device__ uint64_t look_back(unsigned long long* st, uint64_t c, uint64_t agg) 
         uint64_t w = idx >= 0 ? ld_acquire_u64(st + idx) : kFlagInc;
         // wait until every inspected predecessor has published something
         while (__any_sync(0xFFFFFFFFu, (w >> 62) == 0ull)) {
-            if ((w >> 62) == 0ull) w = ld_acquire_u64(st + idx);
+            if ((w >> 62) == 0ull) {
+                __nanosleep(64);
+                w = ld_acquire_u64(st + idx);
+            }
         }
         const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2ull);
         // lanes up to and including the nearest inclusive predecessor contribute
@@ -263,10 +302,13 @@ __device__ uint64_t look_back(unsigned long long* st, uint64_t c, uint64_t agg) 
     return excl;
 }
 
-__global__ void __launch_bounds__(kPT, 2) k_parse_text(ParseParams p) {
+__global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
+    static_assert(kLPT == 1, "one line per thread per round (the pending chunk keeps one result per thread)");
+    constexpr uint32_t kWPT = kChunk / 32u / kPT;       // owned bitmask words per thread
     extern __shared__ __align__(128) uint8_t s_buf[];   // 2 x kBufAlloc
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint16_t s_start[kLCap];
+    __shared__ uint32_t s_nlm[kWords], s_cmm[kWords];   // newline / comma bitmasks of the current chunk
     __shared__ uint32_t s_w[kPT / 32];
     __shared__ uint64_t s_next, s_base[2];
     __shared__ uint32_t s_stat[8];
@@ -286,6 +328,43 @@ __global__ void __launch_bounds__(kPT, 2) k_parse_text(ParseParams p) {
     __syncthreads();
     uint64_t c = s_next;
     uint32_t stage = 0, phase[2] = {0u, 0u};
+    const int64_t tz_ms = (int64_t)p.tz_offset_min * 60000;
+
+    // write one parsed line: status, per-status count, the record (if valid) at output index o
+    auto write_line = [&](const LineOut& r, uint64_t line, uint64_t o) {
+        if (r.status == kNoLine) return;
+        if (p.status && line < p.status_cap) p.status[line] = (uint8_t)r.status;
+        atomicAdd(&s_stat[r.status], 1u);
+        if (r.status == kLineOk) {
+            if (o < p.cap) {
+                p.ts[o] = r.ts;
+                p.src[o] = r.src;
+                p.dst[o] = r.dst;
+                p.bytes[o] = r.bytes;
+            }
+        } else {
+            atomicMin(reinterpret_cast<unsigned long long*>(&s_firstbad), (unsigned long long)line);
+        }
+    };
+
+    // the previous single-round chunk: parsed, aggregates published, look-back + writes pending
+    bool pend = false;
+    uint64_t pc = 0;
+    uint32_t p_lines = 0, p_valid = 0, p_vpre = 0;
+    LineOut pres;
+    pres.status = kNoLine;
+    auto finish_pending = [&]() {   // block-uniform
+        if (!pend) return;
+        if (tid < 32) {
+            const uint64_t lb = finish_look_back(p.st_lines, pc, p_lines);
+            const uint64_t vb = finish_look_back(p.st_valid, pc, p_valid);
+            if (tid == 0) { s_base[0] = lb; s_base[1] = vb; }
+        }
+        __syncthreads();
+        write_line(pres, s_base[0] + tid, s_base[1] + p_vpre);
+        __syncthreads();                               // s_base is rewritten
+        pend = false;
+    };
 
     while (c < p.n_chunks) {
         __syncthreads();                               // everyone has read s_next
@@ -298,114 +377,110 @@ __global__ void __launch_bounds__(kPT, 2) k_parse_text(ParseParams p) {
         phase[stage] ^= 1u;
         const uint8_t* buf = s_buf + stage * kBufAlloc;
         const uint64_t off = c * kChunk;
-        const uint32_t cl = (uint32_t)min((uint64_t)kChunk, p.len - off);       // owned bytes
         const uint32_t staged = (uint32_t)min((uint64_t)kBuf, p.len - off);
-        // newline at chunk-local x starts a line iff off + x < len - 1
-        const uint32_t nl_lim = (uint32_t)min((uint64_t)cl, (uint64_t)(p.len - 1ull - off));
+        // newline at chunk-local x starts a line iff x < kChunk and off + x < len - 1
+        const uint32_t nl_lim = (uint32_t)min((uint64_t)kChunk, (uint64_t)(p.len - 1ull - off));
         const uint32_t head = (c == 0) ? 1u : 0u;      // the line at offset 0
 
-        // ---- lines of this chunk: newlines per thread (16-byte words), block scan
-        constexpr uint32_t kSeg = kChunk / kPT;
-        const uint32_t a0 = tid * kSeg;
-        auto nl_mask = [&](uint32_t a, uint4 v, int k) {
-            const uint32_t w = k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
-            uint32_t m = __vcmpeq4(w, 0x0A0A0A0Au);
-            const uint32_t base = a + 4u * k;
-            if (base + 4u > nl_lim) m &= base >= nl_lim ? 0u : (1u << (8u * (nl_lim - base))) - 1u;
-            return m;
+        // ---- structural index: newline and comma bitmasks of the staged bytes
+        for (uint32_t w = tid; w < kWords; w += kPT) {
+            const uint32_t a = w * 32u;
+            uint32_t nl = 0u, cm = 0u;
+            if (a < staged) {
+                const uint4 v0 = *reinterpret_cast<const uint4*>(buf + a);
+                const uint4 v1 = *reinterpret_cast<const uint4*>(buf + a + 16u);
+                nl = eq_mask32(v0, v1, 0x0A0A0A0Au);
+                cm = eq_mask32(v0, v1, 0x2C2C2C2Cu);
+                if (staged - a < 32u) {
+                    const uint32_t keep = (1u << (staged - a)) - 1u;
+                    nl &= keep;
+                    cm &= keep;
+                }
+            }
+            s_nlm[w] = nl;
+            s_cmm[w] = cm;
+        }
+        __syncthreads();
+
+        // ---- lines of this chunk: the newlines it owns, counted per thread, block scan
+        auto owned = [&](uint32_t w) -> uint32_t {    // bits of word w at chunk-local x < nl_lim
+            const uint32_t b0 = w * 32u;
+            if (b0 + 32u <= nl_lim) return 0xFFFFFFFFu;
+            return b0 >= nl_lim ? 0u : (1u << (nl_lim - b0)) - 1u;
         };
         uint32_t my_nl = 0;
-        for (uint32_t a = a0; a < a0 + kSeg && a < nl_lim; a += 16u) {
-            const uint4 v = *reinterpret_cast<const uint4*>(buf + a);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) my_nl += __popc(nl_mask(a, v, k)) >> 3;
-        }
+        for (uint32_t k = 0; k < kWPT; ++k) my_nl += __popc(s_nlm[tid * kWPT + k] & owned(tid * kWPT + k));
         uint32_t n_lines;
         const uint32_t my_first = block_scan(my_nl, s_w, &n_lines) + head;
         n_lines += head;
-        const int64_t tz_ms = (int64_t)p.tz_offset_min * 60000;
 
-        // ---- parse in rounds of kLCap lines (thread t: lines t*kLPT .. t*kLPT+kLPT-1 of a round)
+        // ---- parse in rounds of kLCap lines (thread t: line t of a round)
         const uint32_t rounds = (n_lines + kLCap - 1u) / kLCap;
-        LineOut res[kLPT];
+        LineOut res;
         auto parse_round = [&](uint32_t r) -> uint32_t {
             const uint32_t r0 = r * kLCap, r1 = min(r0 + kLCap, n_lines);
             if (head && r == 0 && tid == 0) s_start[0] = 0;
             uint32_t idx = my_first;
-            for (uint32_t a = a0; a < a0 + kSeg && a < nl_lim && idx < r1; a += 16u) {
-                const uint4 v = *reinterpret_cast<const uint4*>(buf + a);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    uint32_t m = nl_mask(a, v, k);
-                    while (m) {
-                        const uint32_t bpos = (__ffs(m) - 1u) >> 3;
-                        m &= ~(0xFFu << (8u * bpos));
-                        if (idx >= r0 && idx < r1) s_start[idx - r0] = (uint16_t)(a + 4u * k + bpos + 1u);
-                        ++idx;
-                    }
+            for (uint32_t k = 0; k < kWPT && idx < r1; ++k) {
+                uint32_t m = s_nlm[tid * kWPT + k] & owned(tid * kWPT + k);
+                while (m) {
+                    const uint32_t bpos = __ffs(m) - 1u;
+                    m &= m - 1u;
+                    if (idx >= r0 && idx < r1) s_start[idx - r0] = (uint16_t)((tid * kWPT + k) * 32u + bpos + 1u);
+                    ++idx;
                 }
             }
             __syncthreads();
-            uint32_t my_valid = 0;
-#pragma unroll
-            for (int u = 0; u < kLPT; ++u) {
-                const uint32_t i = r0 + tid * kLPT + u;
-                res[u].status = kNoLine;
-                if (i < r1) {
-                    const uint32_t st = s_start[i - r0];
-                    res[u] = parse_line(buf, st, staged > st ? staged - st : 0u, tz_ms);
-                    my_valid += res[u].status == kLineOk ? 1u : 0u;
-                }
+            const uint32_t i = r0 + tid;
+            res.status = kNoLine;
+            if (i < r1) {
+                const uint32_t st = s_start[i - r0];
+                res = parse_line(buf, s_nlm, s_cmm, st, staged > st ? staged - st : 0u, tz_ms);
             }
             __syncthreads();                           // s_start is rewritten by the next round
-            return my_valid;
+            return res.status == kLineOk ? 1u : 0u;
         };
-        auto write_round = [&](uint32_t r, uint64_t line_base, uint64_t o) {
-            const uint32_t r0 = r * kLCap;
-#pragma unroll
-            for (int u = 0; u < kLPT; ++u) {
-                if (res[u].status == kNoLine) continue;
-                const uint64_t line = line_base + r0 + tid * kLPT + u;
-                if (p.status && line < p.status_cap) p.status[line] = (uint8_t)res[u].status;
-                atomicAdd(&s_stat[res[u].status], 1u);
-                if (res[u].status == kLineOk) {
-                    if (o < p.cap) {
-                        p.ts[o] = res[u].ts;
-                        p.src[o] = res[u].src;
-                        p.dst[o] = res[u].dst;
-                        p.bytes[o] = res[u].bytes;
-                    }
-                    ++o;
-                } else {
-                    atomicMin(reinterpret_cast<unsigned long long*>(&s_firstbad), (unsigned long long)line);
-                }
-            }
-        };
-        auto bases = [&](uint32_t n_valid) {    // decoupled look-back of both counts (warp 0)
-            if (tid < 32) {
-                const uint64_t lb = look_back(p.st_lines, c, n_lines);
-                const uint64_t vb = look_back(p.st_valid, c, n_valid);
-                if (tid == 0) { s_base[0] = lb; s_base[1] = vb; }
-            }
-            __syncthreads();
-        };
-        if (rounds <= 1u) {                    // the common case: parse once, keep results in registers
+        if (rounds <= 1u) {
+            // the common case: parse once, publish the chunk's counts, then finish the previous
+            // chunk (whose predecessors have had a chunk's time to publish) and keep this one
             const uint32_t my_valid = rounds ? parse_round(0) : 0u;
             uint32_t n_valid;
             const uint32_t vpre = block_scan(my_valid, s_w, &n_valid);
-            bases(n_valid);
-            if (rounds) write_round(0, s_base[0], s_base[1] + vpre);
-        } else {                               // very short lines: count every round, then re-parse and write
+            if (tid == 0) {
+                publish_agg(p.st_lines, c, n_lines);
+                publish_agg(p.st_valid, c, n_valid);
+            }
+            finish_pending();
+            pend = true;
+            pc = c;
+            p_lines = n_lines;
+            p_valid = n_valid;
+            p_vpre = vpre;
+            pres = res;
+        } else {
+            // very short lines: count every round, look back, then re-parse and write
+            finish_pending();
             uint32_t n_valid = 0, rv;
             for (uint32_t r = 0; r < rounds; ++r) {
                 block_scan(parse_round(r), s_w, &rv);
                 n_valid += rv;
             }
-            bases(n_valid);
+            if (tid == 0) {
+                publish_agg(p.st_lines, c, n_lines);
+                publish_agg(p.st_valid, c, n_valid);
+            }
+            if (tid < 32) {
+                const uint64_t lb = finish_look_back(p.st_lines, c, n_lines);
+                const uint64_t vb = finish_look_back(p.st_valid, c, n_valid);
+                if (tid == 0) { s_base[0] = lb; s_base[1] = vb; }
+            }
+            __syncthreads();
+            const uint64_t lb = s_base[0];
             uint64_t o = s_base[1];
             for (uint32_t r = 0; r < rounds; ++r) {
                 const uint32_t vpre = block_scan(parse_round(r), s_w, &rv);
-                write_round(r, s_base[0], o + vpre);
+                write_line(res, lb + r * kLCap + tid, o + vpre);
                 o += rv;
             }
         }
@@ -413,6 +488,7 @@ __global__ void __launch_bounds__(kPT, 2) k_parse_text(ParseParams p) {
         c = s_next;
         stage ^= 1u;
     }
+    finish_pending();
     __syncthreads();
     if (tid < 7 && s_stat[tid]) atomicAdd(reinterpret_cast<unsigned long long*>(p.result + 3 + tid),
                                           (unsigned long long)s_stat[tid]);

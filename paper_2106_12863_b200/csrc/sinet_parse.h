@@ -6,7 +6,7 @@
 
 namespace sinet {
 
-constexpr uint32_t kParseChunk = 48u * 1024u;   // text bytes owned by one chunk (look-back unit)
+constexpr uint32_t kParseChunk = 16u * 1024u;   // text bytes owned by one chunk (look-back unit)
 
 // line status codes (= SINET_LINE_* in include/sinet.h)
 constexpr uint32_t kLineOk = 0, kLineLong = 1, kLineColumns = 2, kLineTime = 3, kLineSrc = 4, kLineDst = 5,

@@ -37,13 +37,14 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 
 // Predicated shared-memory updates of one (bin, dir) slot at shared address a (count word;
-// low bytes word at a + 8): if take, count += 1 and low += lo, returning the
+// low bytes word at a + LO): if take, count += 1 and low += lo, returning the
 // low word's old value (0 if not taken).
+template <uint32_t LO>
 __device__ __forceinline__ uint32_t smem_count_and_add_lo(uint32_t a, bool take, uint32_t lo) {
     uint32_t old;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t"
-                 "@q red.shared.add.u32 [%1], 1;\n\t@q atom.shared.add.u32 %0, [%1+8], %3;\n\t}"
-                 : "=r"(old) : "r"(a), "r"((uint32_t)take), "r"(lo) : "memory");
+                 "@q red.shared.add.u32 [%1], 1;\n\t@q atom.shared.add.u32 %0, [%1+%4], %3;\n\t}"
+                 : "=r"(old) : "r"(a), "r"((uint32_t)take), "r"(lo), "n"(LO) : "memory");
     return old;
 }
 
@@ -113,10 +114,8 @@ __device__ void spill_warp(const KernelParams& p, bool need, uint32_t bin, uint3
             const ulonglong2 z = make_ulonglong2(0ull, 0ull);
             for (uint32_t i = lane; i < kTileBins * 2u; i += 32u) b[i] = z;
             __syncwarp();
-            if (lane == 0) {
-                __threadfence();
-                st_release_u32(p.tile_flags + tl, (p.epoch << 2) | kTileInit);
-            }
+            // st.release is cumulative over the warp's zero stores ordered before it by __syncwarp
+            if (lane == 0) st_release_u32(p.tile_flags + tl, (p.epoch << 2) | kTileInit);
         }
         __syncwarp();
         const bool mine = need && t == tl;
@@ -151,8 +150,9 @@ __device__ __forceinline__ uint32_t claim_outcome(uint32_t* flag, uint32_t epoch
     }
 }
 
-// Shared-memory window: a ring of NT tiles x 256 ms bins, 4 u32 per bin =
-// {cnt_out, cnt_in, lo_out, lo_in}: the low 32 bits of the byte sums.  A record whose bytes
+// Shared-memory window: a ring of NT tiles x 256 ms bins, 4 u32 per bin in two arrays,
+// cnt[WS][2 dir] and lo[WS][2 dir] (the low 32 bits of the byte sums): the count words of
+// a warp's 32 records spread over all 32 banks (16 with one 16-byte slot per bin).  A record whose bytes
 // reach the high word (>= 2^32, or a carry out of the low word: elephants, very hot bins)
 // adds that part straight to HBM through the spill path, after the chunk barrier, when
 // the group holds no claim.  A thread retires one bin as one full 32-byte sector, so a
@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // the lookup table is shared.  A group synchronises on its own named barrier.
     const uint32_t gid = threadIdx.x / GT, tid = threadIdx.x % GT, lane = tid & 31u, warp = tid >> 5;
     constexpr uint32_t kSlot = 4;             // u32 per ring bin
-    uint32_t* s_win = smem + gid * (WS * kSlot);
+    uint32_t* s_win = smem + gid * (WS * kSlot);   // cnt[WS][2], then lo[WS][2]
+    constexpr uint32_t kLoOff = WS * 2u;      // u32 offset of the lo array
     uint32_t (*s_red)[2][GW] = s_red_all[gid];
     uint32_t* s_state = s_state_all[gid];
     auto group_sync = [&]() {
@@ -229,18 +230,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // write (won: plain stores) or add (RED) 4 consecutive bins of the ring to HBM and zero them
     // write (won: plain stores) or add (RED) one bin of the ring to HBM and zero it
     auto flush_bin = [&](uint32_t bin, bool won) {
-        uint4* s = reinterpret_cast<uint4*>(s_win + (bin & (WS - 1)) * kSlot);
-        const uint4 v = *s;   // {cnt_out, cnt_in, lo_out, lo_in}
-        *s = make_uint4(0u, 0u, 0u, 0u);
+        uint2* sc = reinterpret_cast<uint2*>(s_win + (bin & (WS - 1)) * 2u);
+        uint2* sl = reinterpret_cast<uint2*>(s_win + kLoOff + (bin & (WS - 1)) * 2u);
+        const uint2 c = *sc, l = *sl;   // {cnt_out, cnt_in}, {lo_out, lo_in}
+        *sc = make_uint2(0u, 0u);
+        *sl = make_uint2(0u, 0u);
         unsigned long long* g64 = p.bins + (size_t)bin * 4u;
         if (won) {
             ulonglong2* g = reinterpret_cast<ulonglong2*>(g64);
-            __stcg(g, make_ulonglong2(v.x, v.z));
-            __stcg(g + 1, make_ulonglong2(v.y, v.w));
+            __stcg(g, make_ulonglong2(c.x, l.x));
+            __stcg(g + 1, make_ulonglong2(c.y, l.y));
         } else {
             // a record with bytes but no count never reaches the ring (counts are >= 1)
-            if (v.x) { atomicAdd(g64, (unsigned long long)v.x); if (v.z) atomicAdd(g64 + 1, (unsigned long long)v.z); }
-            if (v.y) { atomicAdd(g64 + 2, (unsigned long long)v.y); if (v.w) atomicAdd(g64 + 3, (unsigned long long)v.w); }
+            if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (l.x) atomicAdd(g64 + 1, (unsigned long long)l.x); }
+            if (c.y) { atomicAdd(g64 + 2, (unsigned long long)c.y); if (l.y) atomicAdd(g64 + 3, (unsigned long long)l.y); }
         }
     };
 
@@ -273,7 +276,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             if (my_o != 0u) {
                 const uint32_t o = my_o;
                 if (o == kWon) {
-                    __threadfence();
+                    // the release is cumulative over the group's bin stores ordered before it
+                    // by the barrier above (no separate fence)
                     st_release_u32(p.tile_flags + t, (p.epoch << 2) | kTileInit);
                 } else if (o == kBusy) {
                     const uint32_t init = (p.epoch << 2) | kTileInit;
@@ -312,10 +316,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // returns the high word (bytes >> 32 + the carry out of the low word, mod 2^32) that the
     // caller must add to HBM as hi << 32 (exact mod 2^64)
     auto accumulate = [&](uint32_t bin, uint32_t dir, uint32_t cnt, uint64_t bytes) -> uint32_t {
-        uint32_t* s = s_win + (bin & (WS - 1)) * kSlot + dir;
+        uint32_t* s = s_win + (bin & (WS - 1)) * 2u + dir;
         atomicAdd(s, cnt);
         const uint32_t lo = (uint32_t)bytes;
-        const uint32_t old = atomicAdd(s + 2, lo);
+        const uint32_t old = atomicAdd(s + kLoOff, lo);
         return (uint32_t)(bytes >> 32) + ((old + lo < old) ? 1u : 0u);
     };
 
@@ -329,8 +333,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         uint32_t old[RPT];
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const uint32_t a = win_base + ((bin[j] & (WS - 1)) * kSlot + dir[j]) * 4u;
-            old[j] = smem_count_and_add_lo(a, take[j], (uint32_t)by[j]);
+            const uint32_t a = win_base + ((bin[j] & (WS - 1)) * 2u + dir[j]) * 4u;
+            old[j] = smem_count_and_add_lo<kLoOff * 4u>(a, take[j], (uint32_t)by[j]);
         }
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {

@@ -15,7 +15,7 @@ from oracle import core as oracle  # noqa: E402
 from synth import WORKLOADS, records  # noqa: E402
 from synth.sinet_text import session_text, session_text_batched  # noqa: E402
 
-CHUNK = 48 * 1024
+CHUNK = int(P._native.lib.sinet_parse_chunk_bytes())   # the kernel's chunk (look-back unit)
 
 
 def gpu_parse(blob: bytes, tz=540, capacity=None):
@@ -67,7 +67,7 @@ def test_empty_and_tiny_texts():
 
 
 def test_many_tiny_lines_multi_round_chunks():
-    # > 512 lines in a 48 KB chunk: the count-then-rewrite path of the kernel
+    # more lines in a chunk than one round parses: the count-then-rewrite path of the kernel
     rng = random.Random(3)
     good, _ = gen_text(50, bad=0)
     lines = good.split(b"\n")[:-1]

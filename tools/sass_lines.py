@@ -24,6 +24,13 @@ def kernel_and_rows(path):
 
 def mangled_match(name, sass_path):
     """The .text section whose mangled template arguments match ncu's demangled kernel name."""
+    if re.search(r"::(\w+)<", name) is None:   # not a template: the section naming the function
+        base = re.search(r"(\w+)\(", name).group(1)
+        secs = re.findall(r"^\.text\.(\S+):$", open(sass_path).read(), re.M)
+        for s in secs:
+            if base in s:
+                return s
+        raise SystemExit(f"no section for {name}")
     args = re.search(r"<(.*)>", name).group(1).split(",")
     want = "I" + "E".join(("Lb" if "(bool)" in a else "Li") + a.split(")")[-1].strip() for a in args) + "E"
     base = re.search(r"::(\w+)<", name).group(1)
