@@ -26,16 +26,17 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    lib = out or LIB
+    if not force and out is None and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *[f"-D{d}" for d in defines],
            "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            "-Xptxas", "-v" if verbose else "-O3", *sources(), "-o", tmp, "-ldl"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -22,7 +22,9 @@ if not os.path.exists(LIB_PATH) or os.environ.get("SINET_REBUILD") == "1":
         raise ImportError(f"libsinet.so not built at {LIB_PATH} and nvcc build failed ({e}): "
                           "run `python -c 'import __graft_entry__ as g; g.build()'`") from e
 
-lib = ctypes.CDLL(LIB_PATH)
+# A/B experiments only: SINET_LIB_VARIANT=x loads libsinet.x.so (built by tools/build_variant.py)
+_variant = os.environ.get("SINET_LIB_VARIANT")
+lib = ctypes.CDLL(os.path.join(_PKG, f"libsinet.{_variant}.so") if _variant else LIB_PATH)
 
 OK, E_INVAL, E_ALIGN, E_RANGE, E_CUDA, E_NCCL, E_STATE = 0, -1, -2, -3, -4, -5, -6
 ERR_NAMES = {E_INVAL: "E_INVAL", E_ALIGN: "E_ALIGN", E_RANGE: "E_RANGE", E_CUDA: "E_CUDA",

@@ -1027,17 +1027,25 @@ extern "C" int sinet_parse_text(const uint8_t* d_text, uint64_t text_bytes, int3
     p.st_lines = reinterpret_cast<unsigned long long*>(ws + 256);
     p.st_valid = p.st_lines + nch;
     p.n_chunks = nch;
+    p.packed = text_bytes < (1ull << 31) ? 1u : 0u;
+    if (const char* u = std::getenv("SINET_PARSE_UNPACKED")) if (std::atoi(u)) p.packed = 0u;   // test hook
     if (e == cudaSuccess && nch) e = launch_parse_text(p, parse_sm_count(), st);
     unsigned long long h[10] = {0};
     unsigned long long last[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && nch) e = cudaMemcpyAsync(&last[0], p.st_lines + nch - 1, 8, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && nch) e = cudaMemcpyAsync(&last[1], p.st_valid + nch - 1, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && nch && !p.packed)
+        e = cudaMemcpyAsync(&last[1], p.st_valid + nch - 1, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return parse_fail(SINET_E_CUDA, std::string("parse_text: ") + cudaGetErrorString(e));
     const unsigned long long mask = (1ull << 62) - 1;
-    result->lines = last[0] & mask;         // the last chunk's inclusive prefix
-    result->valid = last[1] & mask;
+    if (p.packed) {                         // the last chunk's inclusive prefix: lines << 31 | valid
+        result->lines = (last[0] & mask) >> 31;
+        result->valid = last[0] & ((1ull << 31) - 1);
+    } else {
+        result->lines = last[0] & mask;
+        result->valid = last[1] & mask;
+    }
     result->first_bad_line = h[2];
     for (int k = 0; k < 7; ++k) result->by_status[k] = h[3 + k];
     if (result->valid > out->capacity)

@@ -39,6 +39,7 @@ constexpr uint32_t kLCap = kPT * kLPT;         // lines per round
 constexpr uint32_t kMaxLine = 2047;
 constexpr uint32_t kNoLine = 0xFFu;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+constexpr uint64_t kHalfMask = (1ull << 31) - 1;   // packed look-back word: lines << 31 | valid
 constexpr uint32_t kWords = kBuf / 32u;        // bitmask words of a staged buffer (1 bit per byte)
 static_assert(kChunk % (16 * kPT) == 0, "each thread scans a whole number of 16-byte words");
 static_assert(kBuf % 32u == 0, "whole bitmask words");
@@ -63,13 +64,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ uint64_t ld_acquire_u64(const unsigned long long* p) {
+// Look-back words pack (flag, value) into one u64, and nothing else is read on the strength
+// of them (the records and statuses a chunk writes are consumed after the kernel), so
+// relaxed gpu-scope accesses suffice: no fence per load or publish.
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // thread 0: stage text [off, min(off + kBuf, len)) into buf.  The 16-byte-aligned body
@@ -268,37 +272,54 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* s_w, uint32
 // chunk), when the predecessors have published theirs.
 // publish_agg: thread 0; chunk 0 publishes its inclusive value at once.
 __device__ __forceinline__ void publish_agg(unsigned long long* st, uint64_t c, uint64_t agg) {
-    st_release_u64(st + c, (c == 0 ? kFlagInc : kFlagAgg) | agg);
+    st_relaxed_u64(st + c, (c == 0 ? kFlagInc : kFlagAgg) | agg);
 }
 // finish_look_back: warp 0; returns the exclusive prefix of chunk c (the sum over all
-// earlier chunks) and publishes its inclusive value.  Lane k inspects predecessor
-// (c - 1 - k) of each window of 32.
+// earlier chunks) and publishes its inclusive value.  A window covers 256 predecessors,
+// 8 consecutive ones per lane loaded together (one round trip per window): the nearest
+// chunk with an inclusive value is typically a wave of CTAs (hundreds of chunks) back.
 __device__ uint64_t finish_look_back(unsigned long long* st, uint64_t c, uint64_t agg) {
+    constexpr int kQ = 8;
     const uint32_t lane = threadIdx.x & 31u;
     if (c == 0) return 0;
     uint64_t excl = 0;
     int64_t j = (int64_t)c - 1;
     for (;;) {
-        const int64_t idx = j - (int64_t)lane;
-        uint64_t w = idx >= 0 ? ld_acquire_u64(st + idx) : kFlagInc;
-        // wait until every inspected predecessor has published something
-        while (__any_sync(0xFFFFFFFFu, (w >> 62) == 0ull)) {
-            if ((w >> 62) == 0ull) {
-                __nanosleep(64);
-                w = ld_acquire_u64(st + idx);
-            }
+        uint64_t w[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const int64_t idx = j - (int64_t)lane * kQ - q;   // q = 0: this lane's nearest
+            w[q] = idx >= 0 ? ld_relaxed_u64(st + idx) : kFlagInc;
         }
-        const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2ull);
-        // lanes up to and including the nearest inclusive predecessor contribute
-        const uint32_t upto = inc ? (__ffs(inc) - 1u) : 31u;
-        uint64_t v = (lane <= upto) ? (w & kValMask) : 0ull;
+        // wait until every inspected predecessor has published something
+        for (;;) {
+            bool missing = false;
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) missing |= (w[q] >> 62) == 0ull;
+            if (!__any_sync(0xFFFFFFFFu, missing)) break;
+            __nanosleep(64);
+#pragma unroll
+            for (int q = 0; q < kQ; ++q)
+                if ((w[q] >> 62) == 0ull) w[q] = ld_relaxed_u64(st + (j - (int64_t)lane * kQ - q));
+        }
+        uint32_t incm = 0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) incm |= ((w[q] >> 62) == 2ull ? 1u : 0u) << q;
+        const uint32_t inc_lanes = __ballot_sync(0xFFFFFFFFu, incm != 0u);
+        // everything nearer than the nearest inclusive predecessor, and that one, contributes
+        const uint32_t L = inc_lanes ? (uint32_t)(__ffs(inc_lanes) - 1) : 32u;
+        const uint32_t qinc = incm ? (uint32_t)(__ffs(incm) - 1) : (uint32_t)kQ;
+        uint64_t v = 0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+            if (lane < L || (lane == L && (uint32_t)q <= qinc)) v += w[q] & kValMask;
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
         excl += v;
-        if (inc) break;
-        j -= 32;
+        if (inc_lanes) break;
+        j -= 32 * kQ;
     }
-    if (lane == 0) st_release_u64(st + c, kFlagInc | (excl + agg));
+    if (lane == 0) st_relaxed_u64(st + c, kFlagInc | (excl + agg));
     return excl;
 }
 
@@ -347,6 +368,16 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
         }
     };
 
+    // publish chunk c's (lines, valid) aggregates (thread 0): one packed word when the
+    // text is < 2 GiB (both prefix sums then fit 31 bits), else one word per scan
+    auto publish_counts = [&](uint32_t n_lines, uint32_t n_valid) {
+        if (p.packed) {
+            publish_agg(p.st_lines, c, ((uint64_t)n_lines << 31) | n_valid);
+        } else {
+            publish_agg(p.st_lines, c, n_lines);
+            publish_agg(p.st_valid, c, n_valid);
+        }
+    };
     // the previous single-round chunk: parsed, aggregates published, look-back + writes pending
     bool pend = false;
     uint64_t pc = 0;
@@ -356,8 +387,15 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
     auto finish_pending = [&]() {   // block-uniform
         if (!pend) return;
         if (tid < 32) {
-            const uint64_t lb = finish_look_back(p.st_lines, pc, p_lines);
-            const uint64_t vb = finish_look_back(p.st_valid, pc, p_valid);
+            uint64_t lb, vb;
+            if (p.packed) {   // one scan of (lines << 31 | valid)
+                const uint64_t x = finish_look_back(p.st_lines, pc, ((uint64_t)p_lines << 31) | p_valid);
+                lb = x >> 31;
+                vb = x & kHalfMask;
+            } else {
+                lb = finish_look_back(p.st_lines, pc, p_lines);
+                vb = finish_look_back(p.st_valid, pc, p_valid);
+            }
             if (tid == 0) { s_base[0] = lb; s_base[1] = vb; }
         }
         __syncthreads();
@@ -447,10 +485,7 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
             const uint32_t my_valid = rounds ? parse_round(0) : 0u;
             uint32_t n_valid;
             const uint32_t vpre = block_scan(my_valid, s_w, &n_valid);
-            if (tid == 0) {
-                publish_agg(p.st_lines, c, n_lines);
-                publish_agg(p.st_valid, c, n_valid);
-            }
+            if (tid == 0) publish_counts(n_lines, n_valid);
             finish_pending();
             pend = true;
             pc = c;
@@ -466,13 +501,17 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
                 block_scan(parse_round(r), s_w, &rv);
                 n_valid += rv;
             }
-            if (tid == 0) {
-                publish_agg(p.st_lines, c, n_lines);
-                publish_agg(p.st_valid, c, n_valid);
-            }
+            if (tid == 0) publish_counts(n_lines, n_valid);
             if (tid < 32) {
-                const uint64_t lb = finish_look_back(p.st_lines, c, n_lines);
-                const uint64_t vb = finish_look_back(p.st_valid, c, n_valid);
+                uint64_t lb, vb;
+                if (p.packed) {
+                    const uint64_t x = finish_look_back(p.st_lines, c, ((uint64_t)n_lines << 31) | n_valid);
+                    lb = x >> 31;
+                    vb = x & kHalfMask;
+                } else {
+                    lb = finish_look_back(p.st_lines, c, n_lines);
+                    vb = finish_look_back(p.st_valid, c, n_valid);
+                }
                 if (tid == 0) { s_base[0] = lb; s_base[1] = vb; }
             }
             __syncthreads();

@@ -28,6 +28,7 @@ struct ParseParams {
     unsigned long long* st_valid;      // [n_chunks] look-back words of the valid counts (zeroed)
     unsigned long long* result;        // [10]: lines, valid (host-filled from the look-back), first bad, count[7]
     uint64_t n_chunks;
+    uint32_t packed;                   // 1: len < 2^31, one look-back of (lines << 31 | valid) in st_lines
 };
 
 size_t parse_smem_bytes();

@@ -387,8 +387,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (tid == 0 && kPF && cbase + kPF * CH < r1) prefetch_records(p, cbase + kPF * CH, min(cbase + (kPF + 1) * CH, r1));
 
         // ---- a3-a5: classify and map this chunk (the claims issued last chunk resolve meanwhile)
+        // dir4[j]: 0 / 1 = the record is binned in that direction and still to be accumulated,
+        // 4 | dir = accumulated before the barrier, 3 = not binned (no per-record bool arrays:
+        // they would live in a register as bit fields across the barrier)
         uint32_t bin4[RPT], dir4[RPT];
-        bool binned4[RPT];
         uint32_t tag4 = 0, bmin = 0xFFFFFFFFu, bmax = 0u;
         WarpTotals ctot;   // this chunk's records (RPT == 2: reduced into shared memory below)
         if (kSmemTot) ctot.zero();
@@ -397,7 +399,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 #pragma unroll
         for (int j = 0; j < RPT; ++j) { addr[2 * j] = cur.src[j]; addr[2 * j + 1] = cur.dst[j]; }
         member_batch_tab<kTab, 2 * RPT>(addr, in8, T);
-        bool inw4[RPT];
         // kFull: every record of the chunk is valid (whole chunk in the batch, no watchlist),
         // so the per-record validity tests and masks drop out of the common path
         auto classify = [&](auto kFullTag) {
@@ -418,11 +419,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                     inw = map_bin(cur.ts[j], p, bin);
                 }
                 const bool directed = valid && dir < 2u;
-                binned4[j] = directed && inw;
+                const bool binned = directed && inw;
                 bin4[j] = bin;
-                dir4[j] = dir;
-                inw4[j] = inw;
-                if (binned4[j]) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
+                dir4[j] = binned ? dir : 3u;
+                if (tags_on) tag4 |= (in8[2 * j] | (in8[2 * j + 1] << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
+                if (binned) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
                 if (kAllValid) tt.add_valid(cell, directed && !inw, dir, cur.by[j]);
                 else tt.add(valid, cell, directed && !inw, dir, cur.by[j]);
             }
@@ -430,9 +431,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (full && !kWatch) classify(std::true_type{});
         else classify(std::false_type{});
         if (tags_on && have) {
-#pragma unroll
-            for (int j = 0; j < RPT; ++j)
-                tag4 |= (in8[2 * j] | (in8[2 * j + 1] << 1) | ((inw4[j] ? 0u : 1u) << 2)) << (8 * j);
             if (RPT == 4) store_tags4(p, my_v, tag4);
             else for (int j = 0; j < RPT; ++j) if (vvalid(p, my_v + j)) p.tags[my_v + j - p.head] = (uint8_t)(tag4 >> (8 * j));
         }
@@ -457,15 +455,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         // retired ([lo_t, act_t), claimed after the previous chunk) nor about to be recycled
         // (>= lo_t + NT): retire only touches the slots of [lo_t, act_t).  Warps do this work
         // instead of waiting at the barrier; the rest is accumulated after the retire.
-        bool done4[RPT];
         uint32_t hi4[RPT];   // high words owed to HBM (added after the barrier)
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) { done4[j] = false; hi4[j] = 0u; }
+        for (int j = 0; j < RPT; ++j) hi4[j] = 0u;
         if (!kAgg && have_window) {
+            bool take[RPT];
 #pragma unroll
-            for (int j = 0; j < RPT; ++j)
-                done4[j] = binned4[j] && bin4[j] / kTileBins - act_t < lo_t + NT - act_t;
-            accumulate_n(done4, bin4, dir4, cur.by, hi4);
+            for (int j = 0; j < RPT; ++j) take[j] = dir4[j] < 2u && bin4[j] / kTileBins - act_t < lo_t + NT - act_t;
+            accumulate_n(take, bin4, dir4, cur.by, hi4);
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) dir4[j] |= take[j] ? 4u : 0u;
         }
         bmin = __reduce_min_sync(kFull, bmin);
         bmax = __reduce_max_sync(kFull, bmax);
@@ -512,7 +511,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             bool rest[RPT];
             bool any_rest = false;
 #pragma unroll
-            for (int j = 0; j < RPT; ++j) { rest[j] = binned4[j] && !done4[j]; any_rest |= rest[j]; }
+            for (int j = 0; j < RPT; ++j) { rest[j] = dir4[j] < 2u; any_rest |= rest[j]; }
             if (__any_sync(kFull, any_rest)) accumulate_n(rest, bin4, dir4, cur.by, hi4);
             bool any_hi = false;
 #pragma unroll
@@ -521,12 +520,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
 #pragma unroll
                 for (int j = 0; j < RPT; ++j)
                     if (__any_sync(kFull, hi4[j] != 0u))
-                        spill_warp(p, hi4[j] != 0u, bin4[j], dir4[j], 0u, (uint64_t)hi4[j] << 32);
+                        spill_warp(p, hi4[j] != 0u, bin4[j], dir4[j] & 1u, 0u, (uint64_t)hi4[j] << 32);
             }
         } else
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const bool b = binned4[j] && !done4[j];
+            const bool b = dir4[j] < 2u;
             bool act = b;
             uint32_t cnt = 1u;
             uint64_t byt = cur.by[j];
@@ -567,7 +566,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             const uint32_t hv = hi4[j] + (in_ring ? accumulate(bin4[j], dir4[j], cnt, byt) : 0u);
             const bool out = act && !in_ring;
             if (__any_sync(kFull, out || hv != 0u))
-                spill_warp(p, out || hv != 0u, bin4[j], dir4[j], out ? cnt : 0u, out ? byt : ((uint64_t)hv << 32));
+                spill_warp(p, out || hv != 0u, bin4[j], dir4[j] & 1u, out ? cnt : 0u, out ? byt : ((uint64_t)hv << 32));
         }
         cur = nxt;
 

@@ -101,6 +101,15 @@ def test_lines_across_chunk_boundaries_and_long_lines():
         check_against_oracle(blob[:len(blob) - cut] + b"\n")
 
 
+def test_unpacked_look_back(monkeypatch):
+    """Texts of 2 GiB or more scan lines and valid records in two look-back words per chunk
+    (one packed word below that); the hook forces the two-word path on a small text."""
+    monkeypatch.setenv("SINET_PARSE_UNPACKED", "1")
+    blob, _ = gen_text(20_000, bad=50_000)
+    check_against_oracle(blob)
+    check_against_oracle(b"\n" * (3 * CHUNK + 5))
+
+
 def test_fuzzed_lines():
     good, _ = gen_text(300, bad=0)
     lines = good.split(b"\n")[:-1]
