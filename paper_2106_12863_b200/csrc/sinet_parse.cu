@@ -8,12 +8,12 @@
 // dotted-quad IPv4 ("translated to a 32-bit sequence"), bytes a
 // decimal u64; per-line status, valid lines written in line order.
 //
-// B200 design: one pass over the text in HBM.  Persistent CTAs (several per SM) take
-// 16 KB chunks by ticket; each chunk (+ a 2 KB tail for the line that crosses its
+// B200 design: one pass over the text in HBM.  Persistent CTAs (8 x 128 threads per SM)
+// take 16 KB chunks by ticket; each chunk (+ a 2 KB tail for the line that crosses its
 // end) is staged into shared memory by a TMA bulk copy (cp.async.bulk, mbarrier
-// completion), double buffered so the next chunk streams in while this one is
-// parsed.  A chunk owns the lines that start right after one of its newlines
-// (chunk 0 also the line at offset 0).  Every thread first turns 32-byte words of
+// completion); once it is parsed (results in registers) the next ticket's chunk streams
+// into the same buffer while the previous chunk looks back and writes.  A chunk owns the
+// lines that start right after one of its newlines (chunk 0 also the line at offset 0).  Every thread first turns 32-byte words of
 // the staged text into newline and comma bitmasks (structural index, 1 bit per
 // byte); the CTA counts line starts (block scan); one thread per line then finds
 // the line end and the commas around fields 1, 5, 8 and 21 with popcounts over the
@@ -323,11 +323,14 @@ __device__ uint64_t finish_look_back(unsigned long long* st, uint64_t c, uint64_
     return excl;
 }
 
-__global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
+#ifndef SINET_PARSE_CTAS
+#define SINET_PARSE_CTAS 8   // resident CTAs per SM (registers <= 64 per thread; measured 1.00 ms vs 1.08 at 6)
+#endif
+__global__ void __launch_bounds__(kPT, SINET_PARSE_CTAS) k_parse_text(ParseParams p) {
     static_assert(kLPT == 1, "one line per thread per round (the pending chunk keeps one result per thread)");
     constexpr uint32_t kWPT = kChunk / 32u / kPT;       // owned bitmask words per thread
-    extern __shared__ __align__(128) uint8_t s_buf[];   // 2 x kBufAlloc
-    __shared__ __align__(8) uint64_t s_bar[2];
+    extern __shared__ __align__(128) uint8_t s_buf[];   // kBufAlloc: the staged chunk
+    __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint16_t s_start[kLCap];
     __shared__ uint32_t s_nlm[kWords], s_cmm[kWords];   // newline / comma bitmasks of the current chunk
     __shared__ uint32_t s_w[kPT / 32];
@@ -336,19 +339,26 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
     __shared__ uint64_t s_firstbad;
 
     const uint32_t tid = threadIdx.x;
+    // thread 0: take the next ticket and stage its chunk into the (single) buffer, once every
+    // thread's reads of it are done (the proxy fence orders them before the TMA writes)
+    auto next_chunk = [&]() {
+        const uint64_t cn = atomicAdd(p.ticket, 1ull);
+        s_next = cn;
+        if (cn < p.n_chunks) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            stage_chunk(p, cn * kChunk, s_buf, &s_bar);
+        }
+    };
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        mbar_init(&s_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint64_t c0 = atomicAdd(p.ticket, 1ull);
-        s_next = c0;
-        if (c0 < p.n_chunks) stage_chunk(p, c0 * kChunk, s_buf, &s_bar[0]);
+        next_chunk();
     }
     if (tid < 8) s_stat[tid] = 0;
     if (tid == 0) s_firstbad = ~0ull;
     __syncthreads();
     uint64_t c = s_next;
-    uint32_t stage = 0, phase[2] = {0u, 0u};
+    uint32_t phase = 0;
     const int64_t tz_ms = (int64_t)p.tz_offset_min * 60000;
 
     // write one parsed line: status, per-status count, the record (if valid) at output index o
@@ -405,15 +415,9 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
     };
 
     while (c < p.n_chunks) {
-        __syncthreads();                               // everyone has read s_next
-        if (tid == 0) {                                // next ticket; its chunk streams in meanwhile
-            const uint64_t cn = atomicAdd(p.ticket, 1ull);
-            s_next = cn;
-            if (cn < p.n_chunks) stage_chunk(p, cn * kChunk, s_buf + (stage ^ 1u) * kBufAlloc, &s_bar[stage ^ 1u]);
-        }
-        mbar_wait(&s_bar[stage], phase[stage]);
-        phase[stage] ^= 1u;
-        const uint8_t* buf = s_buf + stage * kBufAlloc;
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        const uint8_t* buf = s_buf;
         const uint64_t off = c * kChunk;
         const uint32_t staged = (uint32_t)min((uint64_t)kBuf, p.len - off);
         // newline at chunk-local x starts a line iff x < kChunk and off + x < len - 1
@@ -485,7 +489,10 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
             const uint32_t my_valid = rounds ? parse_round(0) : 0u;
             uint32_t n_valid;
             const uint32_t vpre = block_scan(my_valid, s_w, &n_valid);
-            if (tid == 0) publish_counts(n_lines, n_valid);
+            if (tid == 0) {
+                publish_counts(n_lines, n_valid);
+                next_chunk();   // the buffer is free: the next chunk streams in during the look-back
+            }
             finish_pending();
             pend = true;
             pc = c;
@@ -522,10 +529,10 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
                 write_line(res, lb + r * kLCap + tid, o + vpre);
                 o += rv;
             }
+            if (tid == 0) next_chunk();
         }
-        __syncthreads();                               // buffer free for the next-but-one stage
+        __syncthreads();                               // s_next is set
         c = s_next;
-        stage ^= 1u;
     }
     finish_pending();
     __syncthreads();
@@ -537,7 +544,7 @@ __global__ void __launch_bounds__(kPT, 5) k_parse_text(ParseParams p) {
 
 }  // namespace
 
-size_t parse_smem_bytes() { return 2u * kBufAlloc; }
+size_t parse_smem_bytes() { return kBufAlloc; }
 
 cudaError_t launch_parse_text(const ParseParams& p, int sm_count, cudaStream_t st) {
     static bool init = false;

@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         unsigned long long* g64 = p.bins + (size_t)bin * 4u;
         if (won) {
             ulonglong2* g = reinterpret_cast<ulonglong2*>(g64);
-            __stcg(g, make_ulonglong2(c.x, l.x));
-            __stcg(g + 1, make_ulonglong2(c.y, l.y));
+            // evict-first: the kernel never re-reads a written bin (measured 1-2 % faster than .cg)
+            __stcs(g, make_ulonglong2(c.x, l.x));
+            __stcs(g + 1, make_ulonglong2(c.y, l.y));
         } else {
             // a record with bytes but no count never reaches the ring (counts are >= 1)
             if (c.x) { atomicAdd(g64, (unsigned long long)c.x); if (l.x) atomicAdd(g64 + 1, (unsigned long long)l.x); }
@@ -646,7 +647,11 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     const int grid = (int)((chunks < (uint64_t)sm_count) ? (chunks ? chunks : 1) : (uint64_t)sm_count);
     const bool w1 = p.width == 1u;
     const int g = stream_groups_for(p);
-    KernelParams q = p;   // ranges: a few per group, each at least a few chunks long
+    KernelParams q = p;
+    // record ranges handed out dynamically, a whole number per group (a partial last wave
+    // leaves most groups idle: C2 with 625 ranges 1.72 ms vs 592 = 2 per group 1.36 ms).
+    // Measured per group: 2 -> C2 1.36 / C4@400M 4.95 / 4 -> 1.37 / 4.39 / 8 -> 1.41 / 4.09 ms
+    // (long ranges save window warm-up and drain, short ones balance bursty stretches): 4.
     const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 4u);
     const uint64_t max_r = p.nv / (4u * 512u * 4u) + 1u;
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
