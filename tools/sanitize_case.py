@@ -21,5 +21,25 @@ for order in ("stream", "shuffled"):
         (ts, c, b), n = h.export_sparse(0)
         h.close()
         print(order, strat, groups, int(t[:4].sum()), int(r.sum()), n)
+# every lookup-table encoding on a /8-/32 list, records with > 2^32 bytes (the ring's high-word spill)
+n5, l5 = prefix_table(WORKLOADS["c5"])
+for tab_nets, tab_lens in ((n5[:100], l5[:100]), (n5, l5)):
+    rec = records(wl.with_(order="stream"), device="cuda")
+    big = rec["bytes"].clone()
+    big[::97] = big[::97] + (1 << 33)
+    for tab in (0, 1, 2, 3):
+        h = S.SinetHistogram(tab_nets, tab_lens, wl.window_start_ms, wl.window_ms, order=1)
+        h.set_table_mode(tab)
+        h.classify(rec["ts"], rec["src"], rec["dst"], big)
+        t = h.read_totals()
+        h.close()
+        print("table", len(tab_nets), tab, int(t[:4].sum()))
+# NEXT-3 parser: several 16 KB chunks, malformed lines, look-back across chunks
+from synth.sinet_text import session_text_batched
+pw = WORKLOADS["c1"].with_(n=3000)
+prec = records(pw, device="cuda")
+text, _ = session_text_batched(pw, prec, bad_per_million=20_000)
+cols, st, info = S.parse_text(text, 540, status=True)
+print("parse", info["lines"], info["valid"])
 torch.cuda.synchronize()
 print("sanitize case done")
