@@ -140,14 +140,18 @@ def cpu_oracle_rate(cols_fn, nets, lens, wl, target_s, threads):
     t0 = time.perf_counter()
     oracle.classify_histogram(*cols, nets, lens, start, window, width, threads=threads, into=res)
     cal = time.perf_counter() - t0
-    n = int(min(wl.n, max(n_cal, n_cal * target_s / max(cal, 1e-3))))
-    if n > n_cal:
-        cols = cols_fn(0, n)
+    n, el = n_cal, cal
+    # the calibration run carries fixed costs (the day of bins), so it over-estimates the
+    # per-record time: re-size from the last run until the sample takes >= 3/4 of the target
+    for _ in range(3):
+        if el >= 0.75 * target_s or n >= wl.n:
+            break
+        n_next = int(min(wl.n, max(n + 1, n * target_s / max(el, 1e-3))))
+        cols = cols_fn(0, n_next)
+        res = oracle.OracleResult(wl.nbins)
         t0 = time.perf_counter()
         oracle.classify_histogram(*cols, nets, lens, start, window, width, threads=threads, into=res)
-        el = time.perf_counter() - t0
-    else:
-        n, el = n_cal, cal
+        n, el = n_next, time.perf_counter() - t0
     return n / el, n, el
 
 

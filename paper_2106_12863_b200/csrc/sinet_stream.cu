@@ -253,22 +253,23 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     auto retire = [&](uint32_t t_from, uint32_t t_to) {
         const uint32_t nt = t_to - t_from;
         if (nt == 0) return;
-        bool busy = false;   // block-uniform: every thread evaluates the same s_state
-        // thread k caches the outcome of tile t_from + k now: after the barrier below,
-        // threads already in the next chunk may re-use the slot for a newer claim
-        uint32_t my_o = 0u;
-        if (tid < nt && touched(t_from + tid)) {
-            const uint32_t t = t_from + tid, st = s_state[t & (NT - 1)];
-            my_o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
+        // lane k of every warp reads the outcome of tile t_from + k once (nt <= NT <= 32); the
+        // warp's ballots give the won / initialised / busy tile masks (group-uniform: every warp
+        // reads the same s_state), walked with ffs.  Thread k (warp 0) keeps its tile's outcome
+        // for pass 2: after the barrier below, threads already in the next chunk may re-use the
+        // slot for a newer claim.
+        uint32_t my_o = 0u, o_l = 0u;
+        if (lane < nt && touched(t_from + lane)) {
+            const uint32_t t = t_from + lane, st = s_state[t & (NT - 1)];
+            o_l = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
         }
+        if (warp == 0u) my_o = o_l;
+        const unsigned won_m = __ballot_sync(kFull, o_l == kWon), init_m = __ballot_sync(kFull, o_l == kInit);
+        const bool busy = __any_sync(kFull, o_l == kBusy);
         // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem
-        for (uint32_t k = 0; k < nt; ++k) {
-            const uint32_t t = t_from + k;
-            if (!touched(t)) continue;
-            const uint32_t st = s_state[t & (NT - 1)];
-            const uint32_t o = ((st >> 2) == t + 1u) ? (st & 3u) : kBusy;
-            if (o == kBusy) { busy = true; continue; }
-            for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin(t * kTileBins + i, o == kWon);
+        for (unsigned m = won_m | init_m; m; m &= m - 1u) {
+            const uint32_t k = (uint32_t)(__ffs(m) - 1);
+            for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin((t_from + k) * kTileBins + i, (won_m >> k) & 1u);
         }
         group_sync();
         // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones
@@ -423,13 +424,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                 const bool binned = directed && inw;
                 bin4[j] = bin;
                 dir4[j] = binned ? dir : 3u;
-                if (tags_on) tag4 |= (in8[2 * j] | (in8[2 * j + 1] << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
+                if (!kAllValid && tags_on)   // tags: the general path only
+                    tag4 |= (in8[2 * j] | (in8[2 * j + 1] << 1) | ((inw ? 0u : 1u) << 2)) << (8 * j);
                 if (binned) { bmin = min(bmin, bin); bmax = max(bmax, bin); }
                 if (kAllValid) tt.add_valid(cell, directed && !inw, dir, cur.by[j]);
                 else tt.add(valid, cell, directed && !inw, dir, cur.by[j]);
             }
         };
-        if (full && !kWatch) classify(std::true_type{});
+        if (full && !kWatch && !tags_on) classify(std::true_type{});   // tags: the general path
         else classify(std::false_type{});
         if (tags_on && have) {
             if (RPT == 4) store_tags4(p, my_v, tag4);
