@@ -896,12 +896,12 @@ int sinet_table_member_host_labelled(const uint32_t* net, const uint8_t* len, co
             const uint32_t y = (ip >> 8) & 0xFFu;
             const uint32_t c2 = (t.l2[(size_t)mi * 16u + (y >> 4)] >> ((y & 15u) * 2u)) & 3u;
             r_packed = (c2 < 2u) ? c2 : search(t.mentry[mi], ip);
-            // packed encoding without level 2: the block's inline entry as stage_stream_table
-            // builds it (<= 3 boundaries as u16 low half - 1, parity at bit 48), else the search
+            // packed encoding without level 2: the block's inline entries as stage_stream_table
+            // builds them (<= 7 boundaries as u16 low half - 1), else the search
             const uint32_t me = t.mentry[mi], lo = me & 0xFFFFu, nb = me >> 16;
-            if (nb <= 3u) {
+            if (nb <= 7u) {
                 uint32_t cnt = 0;
-                for (uint32_t j = 0; j < 3u; ++j) {
+                for (uint32_t j = 0; j < 7u; ++j) {
                     const uint32_t v = (j < nb) ? ((t.bnd[lo + j] & 0xFFFFu) - 1u) : 0xFFFFu;
                     cnt += v < (ip & 0xFFFFu) ? 1u : 0u;
                 }

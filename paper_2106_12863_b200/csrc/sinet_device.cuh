@@ -142,9 +142,10 @@ __device__ __forceinline__ void member_batch_byte(const uint32_t (&ip)[K], uint3
 
 // member() of K addresses with the packed encoding without level 2 (kTabPackedNoL2: large
 // lists whose level 2 does not fit in shared memory, e.g. the 4096-entry C5 list: 2023 mixed
-// /16 blocks with 1.9 boundaries on average).  A mixed /16 with <= 3 boundaries decides from
-// its 8-byte inline entry (one LDS.64, three compares: measured C5 5.67 -> 5.24 ms against
-// the boundary search); a block with more boundaries searches them.
+// /16 blocks with 1.9 boundaries on average).  A mixed /16 with <= 7 boundaries decides from its 16-byte inline entry (one LDS.128, seven compares,
+// branch-free; measured C5 5.67 -> 5.18 ms against searching every mixed block, 5.32 ms with
+// 3 inline boundaries + search, 5.40 ms with a second entry behind a branch); a block with more
+// boundaries searches them.
 template <int K>
 __device__ __forceinline__ void member_batch_nol2(const uint32_t (&ip)[K], uint32_t (&in)[K], const Table& T) {
     uint32_t w[K], r[K];
@@ -165,18 +166,23 @@ __device__ __forceinline__ void member_batch_nol2(const uint32_t (&ip)[K], uint3
         search |= c[k] == 2u;
     }
     if (search) {
-        // inline block entries (stage_stream_table): up to 3 boundaries of the block as
-        // u16 (low half - 1, unused 0xFFFF), the parity of the boundaries before it at bit
-        // 48; bit 63 marks a block with more boundaries (low word = its mentry: search)
-        const unsigned long long* me64 = reinterpret_cast<const unsigned long long*>(T.mentry);
+        // inline block entries (stage_stream_table), 16 bytes per mixed block: its boundaries
+        // 0-6 as u16 (low half - 1; unused slots 0xFFFF, which no low half exceeds) in .x .y .z
+        // and the low half of .w, the parity of the boundaries before the block at .w bit 16,
+        // .w bit 31 = more than 7 boundaries (.x = its mentry: search).  Branch-free: a warp holds
+        // 256 addresses, so a rare loop-carrying path would run in nearly every warp.
+        auto below = [](uint32_t w, uint32_t x) {   // #u16 halves of w below x
+            return ((w & 0xFFFFu) < x ? 1u : 0u) + ((w >> 16) < x ? 1u : 0u);
+        };
+        const uint4* me128 = reinterpret_cast<const uint4*>(T.mentry);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             if (c[k] != 2u) continue;
-            const unsigned long long e = me64[r[k]];
-            const uint32_t lo = (uint32_t)e, hi = (uint32_t)(e >> 32), x = ip[k] & 0xFFFFu;
-            const uint32_t cnt = ((lo & 0xFFFFu) < x ? 1u : 0u) + ((lo >> 16) < x ? 1u : 0u) + ((hi & 0xFFFFu) < x ? 1u : 0u);
-            in[k] = (cnt ^ (hi >> 16)) & 1u;
-            if (hi >> 31) in[k] = block_search(lo, ip[k], T.bnd);
+            const uint4 e = me128[r[k]];
+            const uint32_t x = ip[k] & 0xFFFFu;
+            const uint32_t cnt = below(e.x, x) + below(e.y, x) + below(e.z, x) + ((e.w & 0xFFFFu) < x ? 1u : 0u);
+            in[k] = (cnt ^ (e.w >> 16)) & 1u;
+            if (e.w >> 31) in[k] = block_search(e.x, ip[k], T.bnd);
         }
     }
 }
@@ -443,21 +449,16 @@ __device__ __forceinline__ typename StreamTab<kTab>::T stage_stream_table(const 
     } else if constexpr (kTab == kTabPackedNoL2) {
         Table T = stage_table<false>(p, smem);
         uint32_t* s_me = smem + kClsWords + kRankWords;
-        uint32_t* s_bnd = s_me + 2u * p.n_mixed;
-        unsigned long long* s_me64 = reinterpret_cast<unsigned long long*>(s_me);
+        uint32_t* s_bnd = s_me + 4u * p.n_mixed;
         for (uint32_t i = threadIdx.x; i < p.n_mixed; i += blockDim.x) {
             const uint32_t me = __ldg(p.mentry + i), lo = me & 0xFFFFu, len = me >> 16;
-            unsigned long long e;
-            if (len <= 3u) {
-                e = (unsigned long long)(lo & 1u) << 48;
-                for (uint32_t j = 0; j < 3u; ++j) {
-                    const uint32_t v = (j < len) ? ((__ldg(p.bnd + lo + j) & 0xFFFFu) - 1u) : 0xFFFFu;
-                    e |= (unsigned long long)v << (16u * j);
-                }
-            } else {
-                e = (1ull << 63) | me;
+            uint4 q = make_uint4(me, 0u, 0u, 0x80000000u);   // > 7 boundaries: search
+            if (len <= 7u) {
+                uint32_t v[8];
+                for (uint32_t j = 0; j < 7u; ++j) v[j] = (j < len) ? ((__ldg(p.bnd + lo + j) & 0xFFFFu) - 1u) : 0xFFFFu;
+                q = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | ((lo & 1u) << 16));
             }
-            s_me64[i] = e;
+            reinterpret_cast<uint4*>(s_me)[i] = q;
         }
         for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
         T.l2 = nullptr;

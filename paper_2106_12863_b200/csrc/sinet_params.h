@@ -76,8 +76,8 @@ constexpr unsigned long kMaxTableSmem = (unsigned long)(kClsWords + kRankWords) 
 // Lookup-table encodings of the stream kernel, all staged in shared memory except the last:
 //   BYTE       byte /16 classes (64 KB) + byte /24 classes of the mixed blocks + entries + boundaries
 //   PACKED     2-bit /16 classes + rank + 2-bit /24 level 2 + entries + boundaries
-//   PACKED_NOL2  the same without level 2: a mixed /16 holds up to 3 boundaries inline (one
-//                8-byte entry, decoded branch-free), else searches its boundaries
+//   PACKED_NOL2  the same without level 2: a mixed /16 holds up to 7 boundaries inline (one
+//                16-byte entry, decoded branch-free), else searches its boundaries
 //   GLOBAL     2-bit /16 classes + rank in shared memory, the rest read from global memory
 enum : int { kTabByte = 0, kTabPacked = 1, kTabPackedNoL2 = 2, kTabGlobal = 3 };
 constexpr unsigned long kStreamTableSmem = 96ul * 1024ul;   // next to the 128 KB ring
@@ -86,7 +86,7 @@ inline unsigned long stream_table_bytes(int mode, uint32_t nbnd, uint32_t n_mixe
     switch (mode) {
         case kTabByte: return 65536ul + (((unsigned long)n_mixed * 256u + 15u) & ~15ul) + 16u + tail;
         case kTabPacked: return (unsigned long)(kClsWords + kRankWords) * 4u + (unsigned long)n_mixed * 64u + tail;
-        case kTabPackedNoL2: return (unsigned long)(kClsWords + kRankWords) * 4u + tail + (unsigned long)n_mixed * 4u;   // u64 entries
+        case kTabPackedNoL2: return (unsigned long)(kClsWords + kRankWords) * 4u + tail + (unsigned long)n_mixed * 12u;   // 16-byte entries
         default: return (unsigned long)(kClsWords + kRankWords) * 4u;
     }
 }

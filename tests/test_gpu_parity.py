@@ -125,6 +125,36 @@ def test_table_encodings_parity(S, oracle_lib, table, tab):
     assert g["h"].table_mode == (2 if table == "c5" and tab in (0, 1) else tab)
 
 
+def _crowded_blocks_table():
+    """Mixed /16 blocks with 1, 2, 3 (inline entry), 4-7 (second inline entry) and 8-20
+    boundaries (boundary search) of the no-level-2 encoding, beside whole /16s and /8s."""
+    nets, lens = [], []
+    for b, k in enumerate((1, 2, 3, 4, 5, 6, 7, 8, 9, 20)):
+        base = (133 << 24) | ((10 + b) << 16)
+        # k boundaries: k // 2 separated /28s, plus one /28 running to the block end if k is odd
+        for j in range(k // 2):
+            nets.append(base | (j * 0x1000 + 0x20)); lens.append(28)
+        if k % 2:
+            nets.append(base | 0xFFF0); lens.append(28)
+    nets += [(150 << 24) | (1 << 16), 10 << 24]; lens += [16, 8]
+    return np.asarray(nets, np.uint32), np.asarray(lens, np.uint8)
+
+
+@pytest.mark.parametrize("groups", [1, 2])
+def test_inline_block_entries_parity(S, oracle_lib, groups):
+    """kTabPackedNoL2 forced: every inline-entry case bit-exact against the oracle (tags too)."""
+    nets, lens = _crowded_blocks_table()
+    start, window = 1_613_660_400_000, 1_000_000
+    for n in (257, 80_003):
+        cols = _adversarial(n, nets, lens, start, window, seed=n + groups)
+        cols = (np.sort(cols[0]),) + cols[1:]
+        g = gpu_run(S, nets, lens, cols, start, window, order=1, tags=True, groups=groups, tab=2)
+        assert g["h"].table_mode == 2
+        assert_parity(g, oracle_lib.classify_histogram(*cols, nets, lens, start, window, 1))
+        np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
+                                                                 start, window))
+
+
 @pytest.mark.parametrize("wl_name,order", [("c1", "stream"), ("c1", "shuffled")])
 def test_c1_full_parity(S, oracle_lib, wl_name, order):
     """BASELINE configs[0] at full size: 1M sessions, 1 h of 1 ms bins, 16 prefixes."""

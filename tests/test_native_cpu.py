@@ -149,3 +149,15 @@ def test_labelled_lpm_table_matches_oracle(oracle_lib, seed):
     l2 = np.array([8, 8], np.uint8)
     assert table_member_host(n2, l2, [0x85010203], [1, 0]).tolist() == [0]
     assert table_member_host(n2, l2, [0x85010203], [0, 1]).tolist() == [1]
+
+
+def test_compiled_table_crowded_blocks(oracle_lib):
+    """Mixed /16 blocks with 1-9 and 20 boundaries: every inline-entry case of the no-level-2
+    encoding (mirrored inside table_member_host) == the oracle's linear scan."""
+    from tests.test_gpu_parity import _crowded_blocks_table
+    nets, lens = _crowded_blocks_table()
+    rng = np.random.default_rng(7)
+    ips = np.concatenate([edge_addresses(nets, lens),
+                          ((133 << 24) | rng.integers(0, 1 << 24, 50_000)).astype(np.uint32)])
+    exp = oracle_lib.tags(np.zeros(len(ips), np.uint64), ips, ips, nets, lens, 0, 1) & 1
+    np.testing.assert_array_equal(table_member_host(nets, lens, ips), exp)
