@@ -18,6 +18,7 @@ struct Table {
     const uint32_t* l2;      // smem (small lists) or global
     const uint32_t* mentry;  // smem (small lists) or global
     const uint32_t* bnd;     // smem (small lists) or global
+    bool any_long = true;    // kTabPackedNoL2: some mixed /16 has more than 7 boundaries
 };
 
 // member(ip): 1 LDS for a /16 wholly in or out; a mixed /16 finds its index m among the
@@ -108,6 +109,7 @@ struct TableB {
     const uint8_t* b24;      // smem [n_mixed * 256 (>= 16)]: 0 / 1 / 2 (mixed /24: search)
     const uint32_t* mentry;  // smem
     const uint32_t* bnd;     // smem
+    bool any_sub24 = true;   // some boundary is not /24-aligned (a prefix longer than /24)
 };
 
 // member() of K addresses with the byte encoding: K byte loads of the /16 classes, then K
@@ -122,18 +124,16 @@ __device__ __forceinline__ void member_batch_byte(const uint32_t (&ip)[K], uint3
 #pragma unroll
     for (int k = 0; k < K; ++k) c[k] = T.b16[ip[k] >> 16];
     uint32_t m[K];
-    bool search = false;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const bool mixed = c[k] >= 2u;
         m[k] = c[k] - 2u;
         const uint32_t c2 = T.b24[mixed ? ((m[k] << 8) | ((ip[k] >> 8) & 0xFFu)) : 0u];
         c[k] = mixed ? c2 : c[k];
-        search |= c[k] == 2u;
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) in[k] = c[k] & 1u;
-    if (search) {
+    if (T.any_sub24) {   // CTA-uniform: only a list with prefixes longer than /24 has mixed /24s
 #pragma unroll
         for (int k = 0; k < K; ++k)
             if (c[k] == 2u) in[k] = block_search(T.mentry[m[k]], ip[k], T.bnd);
@@ -142,10 +142,12 @@ __device__ __forceinline__ void member_batch_byte(const uint32_t (&ip)[K], uint3
 
 // member() of K addresses with the packed encoding without level 2 (kTabPackedNoL2: large
 // lists whose level 2 does not fit in shared memory, e.g. the 4096-entry C5 list: 2023 mixed
-// /16 blocks with 1.9 boundaries on average).  A mixed /16 with <= 7 boundaries decides from its 16-byte inline entry (one LDS.128, seven compares,
-// branch-free; measured C5 5.67 -> 5.18 ms against searching every mixed block, 5.32 ms with
-// 3 inline boundaries + search, 5.40 ms with a second entry behind a branch); a block with more
-// boundaries searches them.
+// /16 blocks with 1.9 boundaries on average).  A mixed /16 with <= 7 boundaries decides from
+// its 16-byte inline entry (one LDS.128, seven compares, branch-free; measured C5 5.67 -> 5.18
+// ms against searching every mixed block, 5.32 ms with 3 inline boundaries + search, 5.40 ms
+// with a second entry behind a branch); a block with more boundaries searches them, in a
+// second pass taken only if the list has such a block (a CTA-uniform flag set while staging:
+// C5 5.18 -> 5.03 ms without the per-address check).
 template <int K>
 __device__ __forceinline__ void member_batch_nol2(const uint32_t (&ip)[K], uint32_t (&in)[K], const Table& T) {
     uint32_t w[K], r[K];
@@ -182,7 +184,14 @@ __device__ __forceinline__ void member_batch_nol2(const uint32_t (&ip)[K], uint3
             const uint32_t x = ip[k] & 0xFFFFu;
             const uint32_t cnt = below(e.x, x) + below(e.y, x) + below(e.z, x) + ((e.w & 0xFFFFu) < x ? 1u : 0u);
             in[k] = (cnt ^ (e.w >> 16)) & 1u;
-            if (e.w >> 31) in[k] = block_search(e.x, ip[k], T.bnd);
+        }
+        if (T.any_long) {   // CTA-uniform: the list has a mixed /16 with more than 7 boundaries
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (c[k] != 2u) continue;
+                const uint4 e = me128[r[k]];
+                if (e.w >> 31) in[k] = block_search(e.x, ip[k], T.bnd);
+            }
         }
     }
 }
@@ -440,7 +449,13 @@ __device__ __forceinline__ typename StreamTab<kTab>::T stage_stream_table(const 
         uint32_t* s_me = reinterpret_cast<uint32_t*>(s24 + n24);
         uint32_t* s_bnd = s_me + p.n_mixed;
         for (uint32_t i = threadIdx.x; i < p.n_mixed; i += blockDim.x) s_me[i] = __ldg(p.mentry + i);
-        for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
+        int sub24 = 0;
+        for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) {
+            const uint32_t b = __ldg(p.bnd + i);
+            s_bnd[i] = b;
+            sub24 |= (b & 0xFFu) != 0u ? 1 : 0;
+        }
+        T.any_sub24 = __syncthreads_or(sub24) != 0;
         T.b16 = reinterpret_cast<const uint8_t*>(s4);
         T.b24 = reinterpret_cast<const uint8_t*>(s24);
         T.mentry = s_me;
@@ -450,8 +465,10 @@ __device__ __forceinline__ typename StreamTab<kTab>::T stage_stream_table(const 
         Table T = stage_table<false>(p, smem);
         uint32_t* s_me = smem + kClsWords + kRankWords;
         uint32_t* s_bnd = s_me + 4u * p.n_mixed;
+        int long_here = 0;
         for (uint32_t i = threadIdx.x; i < p.n_mixed; i += blockDim.x) {
             const uint32_t me = __ldg(p.mentry + i), lo = me & 0xFFFFu, len = me >> 16;
+            long_here |= len > 7u ? 1 : 0;
             uint4 q = make_uint4(me, 0u, 0u, 0x80000000u);   // > 7 boundaries: search
             if (len <= 7u) {
                 uint32_t v[8];
@@ -462,6 +479,7 @@ __device__ __forceinline__ typename StreamTab<kTab>::T stage_stream_table(const 
         }
         for (uint32_t i = threadIdx.x; i < p.nbnd; i += blockDim.x) s_bnd[i] = __ldg(p.bnd + i);
         T.l2 = nullptr;
+        T.any_long = __syncthreads_or(long_here) != 0;
         T.mentry = s_me;
         T.bnd = s_bnd;
         return T;
