@@ -121,7 +121,7 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes, int world) {
     L.mentry = off; off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 4, 256);
     L.l2 = off;     off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 64, 256);
     L.b16 = off;    off = align_up(off + 65536, 256);
-    L.b24 = off;    off = align_up(off + (size_t)kMaxByteMixed * 256, 256);
+    L.b24 = off;    off = align_up(off + (size_t)kMaxByteMixed * 256 + 16, 256);   // + the 16 B the staging over-reads
     L.flags = off;  off = align_up(off + (size_t)n_tiles * 4, 256);
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
     L.counters = off; off = align_up(off + 64, 256);   // [0] range counter, [4..5] touched min/max
@@ -478,6 +478,9 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.l2, c->table.l2.data(), c->table.l2.size() * 4, cudaMemcpyHostToDevice, c->stream));
     if (!c->table.b16.empty())
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.b16, c->table.b16.data(), 65536, cudaMemcpyHostToDevice, c->stream));
+    // the stream kernel stages b24 in whole 16-byte words plus one (b24[0] is always read):
+    // zero the bytes past the table so that every staged byte is initialised
+    OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.b24 + c->table.b24.size(), 0, 16, c->stream));
     if (!c->table.b24.empty())
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.b24, c->table.b24.data(), c->table.b24.size(), cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.flags, 0, (size_t)g.n_tiles * 4, c->stream));
