@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SINET_ABI_VERSION 1
+#define SINET_ABI_VERSION 2
 
 /* error codes */
 #define SINET_OK        0
@@ -66,6 +66,7 @@ extern "C" {
 #define SINET_ORDER_SHUFFLED  2   /* arbitrary order: prefill bins, then L2 atomics */
 
 typedef struct sinet_ctx sinet_ctx;
+typedef struct sinet_hub sinet_hub;   /* in-process rendezvous of the ranks of one merge (see sinet_hub_create) */
 
 /* One batch ("chunk") of session records, columnar.
  * Device pointers for sinet_classify_histogram: naturally aligned, and all four
@@ -207,6 +208,20 @@ int sinet_comm_init(sinet_ctx* ctx, const void* nccl_unique_id);
  * ranks before sinet_comm_init.  Errors: E_NCCL, E_INVAL (NULL out). */
 int sinet_nccl_unique_id(void* out128);
 
+/* In-process merge, the paper's own layout ("we assign one thread for each GPU"):
+ * `world` ctxs in ONE process -- on distinct GPUs, or several on one GPU -- join a hub
+ * instead of NCCL; each rank then calls sinet_reduce from its own host thread (the calls
+ * rendezvous on a host barrier; device order is kept with CUDA events).  Data moves by
+ * peer copies over UVA, and the dense reduce-scatter is one kernel per owner reading its
+ * slice from every rank's bins directly (NVLink P2P loads between GPUs; peer access is
+ * enabled on first use).  Results are identical to the NCCL path.  The hub must outlive
+ * every ctx attached to it; a ctx attaches once (sinet_close detaches it).
+ * Errors: E_INVAL (world < 1 or > 64, NULL out / hub, hub world != cfg.world, rank already
+ * attached), E_STATE (ctx already has a communicator). */
+int sinet_hub_create(sinet_hub** out, int32_t world);
+void sinet_hub_destroy(sinet_hub* hub);
+int sinet_comm_init_hub(sinet_ctx* ctx, sinet_hub* hub);
+
 /* Merge the per-GPU partial histograms (merge-scatter): finalize,
  * then an in-place reduce-scatter (u64 sum) leaves rank g the global sums of
  * bins [g*B_pad/world, (g+1)*B_pad/world); totals are all-reduced so every
@@ -247,11 +262,15 @@ int sinet_read_bins(sinet_ctx* ctx, int dir, int metric, uint64_t first_bin, uin
                     uint64_t* dst, int dst_is_device);
 
 /* NEXT-1, coarser frames: "Session data is grouped into one-hour frame bins"
- * (P:L323); "about 40,000 in 10 minutes".  Sums every `factor`
- * consecutive bins of the owned range [lo, lo+n) into
- * d_out u64[n_out][2 dir][2 metric] (device, 8-byte aligned), coarse bin k =
- * bins [lo + k*factor, min(lo + (k+1)*factor, lo+n)); n_out must equal
- * ceil(n / factor).  u64 sums wrap mod 2^64.  Errors: E_INVAL, E_CUDA. */
+ * (P:L323); "about 40,000 in 10 minutes".  Frame F = bins
+ * [F*factor, (F+1)*factor) of the window (frames aligned to window_start).  The
+ * owned range [lo, lo+n) meets frames first_frame = floor(lo/factor) ..
+ * ceil((lo+n)/factor) - 1 (sinet_rebin_frames); sinet_rebin writes, for each, the sum
+ * of its OWNED bins into d_out u64[n_frames][2 dir][2 metric] (device, 8-byte
+ * aligned), d_out[k] = frame first_frame + k.  A frame that straddles two ranks'
+ * owned ranges is the sum of their two entries for it.  n_out must equal
+ * n_frames.  u64 sums wrap mod 2^64.  Errors: E_INVAL, E_CUDA. */
+int sinet_rebin_frames(sinet_ctx* ctx, uint64_t factor, uint64_t* first_frame, uint64_t* n_frames);
 int sinet_rebin(sinet_ctx* ctx, uint64_t factor, uint64_t* d_out, uint64_t n_out);
 
 /* NEXT-1, sparse series: the key/value namespaces X1<timestamp>, X1<count>,
@@ -350,6 +369,12 @@ int sinet_table_member_host_labelled(const uint32_t* prefix_net, const uint8_t* 
  * stream_groups 0 = automatic, 1 = one 8192-bin ring per CTA, 2 = two independent
  * 4096-bin rings per CTA; warp_aggregation 1/0 = on/off, -1 = unchanged.  Errors: E_INVAL. */
 int sinet_set_tuning(sinet_ctx* ctx, int stream_groups, int warp_aggregation);
+/* Named performance knobs (results are identical for every setting; they exist for A/B
+ * measurements and tests): "stream_groups" 0..2, "warp_aggregation" 0/1,
+ * "ranges_per_group" 0..64 (0 = default), "l2_prefetch_chunks" 0..8, "table_mode" -1..3
+ * (as sinet_set_table_mode), "exchange" 0..2 (as sinet_set_exchange).
+ * Errors: E_INVAL (unknown name or value out of range). */
+int sinet_set_knob(sinet_ctx* ctx, const char* name, int64_t value);
 /* Lookup-table encoding of the STREAM kernel (Alg. 1 l.6-9 compiled by sinet_open;
  * results are identical for every setting): -1 = automatic (the fastest that fits
  * in shared memory), 0 = byte /16 + /24 classes, 1 = packed 2-bit classes with

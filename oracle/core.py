@@ -61,6 +61,9 @@ def _load():
         lib.oracle_histogram_members.argtypes = [u64p, u8p, u8p, u64p, ctypes.c_uint64, ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.c_uint32, u8p, u64p, u64p, u64p]
         lib.oracle_histogram_members.restype = None
+        lib.oracle_member_bylen_batch.argtypes = [u32p, ctypes.c_uint64, u32p, u8p, ctypes.c_uint32, u8p,
+                                                  ctypes.c_int]
+        lib.oracle_member_bylen_batch.restype = ctypes.c_int
         lib.oracle_member_lpm_batch.argtypes = [u32p, ctypes.c_uint64, u32p, u8p, u8p, ctypes.c_uint32, u8p]
         lib.oracle_member_lpm_batch.restype = None
         lib.oracle_watch_filter.argtypes = [u32p, u32p, ctypes.c_uint64, u32p, ctypes.c_uint32, u64p]
@@ -212,6 +215,38 @@ def classify_histogram_watched(ts, src, dst, nbytes, nets, lens, watchlist, star
     keep = watch_filter(src, dst, watchlist)
     cols = [np.ascontiguousarray(np.asarray(c)[keep]) for c in (ts, src, dst, nbytes)]
     return classify_histogram(*cols, nets, lens, start, window, width, lut=lut, threads=threads)
+
+
+def member_bylen(ips, nets, lens, threads: int = 1) -> np.ndarray:
+    """Membership of every address (0/1), Alg. 1 l.4-9 grouped by Z (oracle_member_bylen_batch)."""
+    ips = np.ascontiguousarray(np.asarray(ips, dtype=np.uint32))
+    nets, lens = _table(nets, lens)
+    out = np.zeros(len(ips), np.uint8)
+    rc = _load().oracle_member_bylen_batch(_ptr(ips, ctypes.c_uint32), len(ips), _ptr(nets, ctypes.c_uint32),
+                                           _ptr(lens, ctypes.c_uint8), len(nets), _ptr(out, ctypes.c_uint8),
+                                           int(threads))
+    if rc != 0:
+        raise RuntimeError("oracle_member_bylen_batch failed")
+    return out
+
+
+def histogram_members(ts, s_in, d_in, nbytes, start: int, window: int, width: int, lut=LUT_SRC_PRIORITY,
+                      into: OracleResult | None = None) -> OracleResult:
+    """The histogram steps after discrimination with the memberships given per record
+    (oracle_histogram_members); accumulates into ``into`` if given."""
+    ts = np.ascontiguousarray(ts, dtype=np.uint64)
+    nbytes = np.ascontiguousarray(nbytes, dtype=np.uint64)
+    s_in = np.ascontiguousarray(s_in, dtype=np.uint8)
+    d_in = np.ascontiguousarray(d_in, dtype=np.uint8)
+    assert len(ts) == len(s_in) == len(d_in) == len(nbytes)
+    res = into if into is not None else OracleResult(window // width)
+    assert res.nbins == window // width
+    lut_a = np.ascontiguousarray(np.asarray(lut, dtype=np.uint8))
+    _load().oracle_histogram_members(_ptr(ts, ctypes.c_uint64), _ptr(s_in, ctypes.c_uint8), _ptr(d_in, ctypes.c_uint8),
+                                     _ptr(nbytes, ctypes.c_uint64), len(ts), start, window, width,
+                                     _ptr(lut_a, ctypes.c_uint8), _ptr(res.count, ctypes.c_uint64),
+                                     _ptr(res.bytes, ctypes.c_uint64), _ptr(res.totals, ctypes.c_uint64))
+    return res
 
 
 def member_lpm(ips, nets, lens, labels) -> np.ndarray:

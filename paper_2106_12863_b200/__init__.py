@@ -12,7 +12,7 @@ from ._native import (  # noqa: F401
     METRIC_COUNT, ORDER_AUTO, ORDER_SHUFFLED, ORDER_STREAM, SinetError,
 )
 from .histogram import (  # noqa: F401
-    SinetHistogram, exchange_plan, owned_bin_range, padded_bins, parse_text, shard_range, table_member_host,
+    SinetHistogram, SinetHub, exchange_plan, owned_bin_range, padded_bins, parse_text, shard_range, table_member_host,
 )
 
 __version__ = "0.1.0"

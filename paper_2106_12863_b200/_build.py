@@ -1,9 +1,13 @@
-"""Build libsinet.so in-tree with nvcc for sm_100a (called by __graft_entry__.build())."""
+"""Build libsinet.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
+
+Each source is compiled to an object in parallel (build/obj), then linked."""
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -17,24 +21,48 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
+def headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                  + [os.path.join(ROOT, "include", "sinet.h")])
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) \
-        + [os.path.join(ROOT, "include", "sinet.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    return any(os.path.getmtime(d) > t for d in sources() + headers())
+
+
+def _flags(defines, verbose):
+    return [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *[f"-D{d}" for d in defines],
+            "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+            "-Xptxas", "-v" if verbose else "-O3"]
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     lib = out or LIB
     if not force and out is None and not stale():
         return LIB
+    flags = _flags(defines, verbose)
+    tag = hashlib.sha1(" ".join(flags).encode()).hexdigest()[:10]
+    objdir = os.path.join(ROOT, "build", "obj", tag)
+    os.makedirs(objdir, exist_ok=True)
+    hdr_t = max(os.path.getmtime(h) for h in headers())
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+            return obj
+        tmp = obj + f".tmp{os.getpid()}"
+        subprocess.check_call([NVCC, *flags, "-c", src, "-o", tmp])
+        os.replace(tmp, obj)
+        return obj
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, srcs))
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *[f"-D{d}" for d in defines],
-           "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-Xptxas", "-v" if verbose else "-O3", *sources(), "-o", tmp, "-ldl"]
-    subprocess.check_call(cmd)
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp, "-ldl"])
     os.replace(tmp, lib)
     return lib
 

@@ -90,6 +90,11 @@ _SIGS = {
     "sinet_read_bins": ([_vp, _i, _i, _u64, _u64, _vp, _i], _i),
     "sinet_read_totals": ([_vp, ctypes.POINTER(Totals)], _i),
     "sinet_rebin": ([_vp, _u64, _vp, _u64], _i),
+    "sinet_rebin_frames": ([_vp, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i),
+    "sinet_hub_create": ([ctypes.POINTER(_vp), ctypes.c_int32], _i),
+    "sinet_hub_destroy": ([_vp], None),
+    "sinet_comm_init_hub": ([_vp, _vp], _i),
+    "sinet_set_knob": ([_vp, ctypes.c_char_p, ctypes.c_int64], _i),
     "sinet_sortreduce_scratch_bytes": ([_CP, _u64], ctypes.c_size_t),
     "sinet_classify_histogram_sortreduce": ([_vp, ctypes.POINTER(Records), _vp, ctypes.c_size_t], _i),
     "sinet_export_sparse": ([_vp, _i, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i),
@@ -118,6 +123,17 @@ for _name, (_args, _res) in _SIGS.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
+
+
+def _header_abi_version() -> int:
+    with open(HEADER) as f:
+        m = re.search(r"#define\s+SINET_ABI_VERSION\s+(\d+)", f.read())
+    return int(m.group(1)) if m else -1
+
+
+if int(lib.sinet_abi_version()) != _header_abi_version():
+    raise ImportError(f"{LIB_PATH} has ABI {int(lib.sinet_abi_version())} but include/sinet.h declares "
+                      f"{_header_abi_version()}: the library is stale, rebuild it (__graft_entry__.build())")
 
 
 def header_functions():

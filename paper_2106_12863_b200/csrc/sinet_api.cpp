@@ -3,7 +3,6 @@
 #include "sinet.h"
 
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 
 #include <algorithm>
 #include <atomic>
@@ -14,62 +13,13 @@
 #include <vector>
 
 #include "prefix_compile.h"
+#include "sinet_comm.h"
 #include "sinet_kernels.h"
 #include "sinet_parse.h"
 
 using namespace sinet;
 
 namespace {
-
-// ------------------------------------------------------------------ NCCL (run-time loaded)
-// Minimal declarations of the NCCL 2.x C API (values from nccl.h 2.28).
-typedef struct ncclComm* ncclComm_t;
-typedef struct { char internal[128]; } ncclUniqueId;
-typedef int ncclResult_t;
-constexpr int kNcclSum = 0;
-constexpr int kNcclUint32 = 3;
-constexpr int kNcclUint64 = 5;
-
-struct NcclApi {
-    bool loaded = false;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*GroupStart)() = nullptr;
-    ncclResult_t (*GroupEnd)() = nullptr;
-    const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-NcclApi* nccl_api(std::string* err) {
-    static NcclApi api;
-    if (api.loaded) return &api;
-    // prefer the libnccl.so.2 already mapped into the process (torch's), else load by name
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) { *err = std::string("cannot load libnccl.so.2: ") + dlerror(); return nullptr; }
-#define SINET_SYM(field, name) \
-    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name)); \
-    if (!api.field) { *err = std::string("libnccl.so.2 lacks ") + name; return nullptr; }
-    SINET_SYM(GetUniqueId, "ncclGetUniqueId")
-    SINET_SYM(CommInitRank, "ncclCommInitRank")
-    SINET_SYM(CommDestroy, "ncclCommDestroy")
-    SINET_SYM(ReduceScatter, "ncclReduceScatter")
-    SINET_SYM(AllReduce, "ncclAllReduce")
-    SINET_SYM(AllGather, "ncclAllGather")
-    SINET_SYM(Send, "ncclSend")
-    SINET_SYM(Recv, "ncclRecv")
-    SINET_SYM(GroupStart, "ncclGroupStart")
-    SINET_SYM(GroupEnd, "ncclGroupEnd")
-    SINET_SYM(GetErrorString, "ncclGetErrorString")
-#undef SINET_SYM
-    api.loaded = true;
-    return &api;
-}
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -98,7 +48,8 @@ bool check_cfg(const sinet_config* c, std::string* err, Geometry* g) {
 }
 
 struct WsLayout {
-    size_t totals, cls2, entry, bnd, rank, mentry, l2, b16, b24, flags, sparse, counters, xranges, staging, staging_bytes, total;
+    size_t totals, cls2, bnd, rank, mentry, l2, b16, b24, flags, sparse, counters, xranges, xtotals, staging,
+        staging_bytes, total;
 };
 
 // Device staging for the sparse multi-GPU exchange: a quarter of the owned slice, capped.
@@ -115,7 +66,6 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes, int world) {
     size_t off = 0;
     L.totals = off; off = align_up(off + 16 * 8, 256);
     L.cls2 = off;   off = align_up(off + (size_t)kClsWords * 4, 256);
-    L.entry = off;  off = align_up(off + 65536 * 4, 256);
     L.bnd = off;    off = align_up(off + ((size_t)4 * n_prefixes + 2) * 4, 256);
     L.rank = off;   off = align_up(off + (size_t)kRankWords * 4, 256);
     L.mentry = off; off = align_up(off + (size_t)(4u * n_prefixes + 2u) * 4, 256);
@@ -126,6 +76,7 @@ WsLayout ws_layout(uint64_t n_tiles, uint32_t n_prefixes, int world) {
     L.sparse = off; off = align_up(off + 16 + (size_t)sparse_blocks(n_tiles * kTileBins) * 4, 256);
     L.counters = off; off = align_up(off + 64, 256);   // [0] range counter, [4..5] touched min/max
     L.xranges = off; off = align_up(off + (size_t)world * 8, 256);
+    L.xtotals = off; off = align_up(off + (size_t)(world > 1 ? world : 0) * 12 * 8, 256);   // in-process all-reduce
     L.staging_bytes = exchange_staging_bytes(n_tiles, world);
     L.staging = off; off = align_up(off + L.staging_bytes, 256);
     L.total = off;
@@ -156,7 +107,6 @@ struct sinet_ctx {
     bool agg = false;             // warp aggregation of equal keys in the stream kernel (measured slower on C4)
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t ranges_per_group = 0;
-    uint32_t stream_threads = 0;
     uint32_t pf_chunks = 0;           // L2 bulk prefetch distance (measured: off is fastest, C2 1.43 vs 1.46 ms)
     int tab_mode = -1;            // stream kernel lookup-table encoding: -1 automatic, 0..3 forced
     int exchange = 0;             // multi-GPU merge: 0 auto (sparse when cheaper), 1 dense, 2 sparse
@@ -166,7 +116,7 @@ struct sinet_ctx {
     const uint32_t* wlist = nullptr;
     uint32_t wn = 0;
     uint64_t launches = 0;
-    ncclComm_t comm = nullptr;
+    std::unique_ptr<Transport> comm;   // cross-GPU merge: NCCL or the in-process hub (sinet_comm.h)
     // host-streaming pipeline
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_done[2] = {nullptr, nullptr};
@@ -216,7 +166,6 @@ KernelParams base_params(sinet_ctx* c) {
     p.totals = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.totals);
     p.tile_flags = ws_u32(c, c->ws.flags);
     p.cls2 = ws_u32(c, c->ws.cls2);
-    p.entry = ws_u32(c, c->ws.entry);
     p.bnd = ws_u32(c, c->ws.bnd);
     p.rank = ws_u32(c, c->ws.rank);
     p.mentry = ws_u32(c, c->ws.mentry);
@@ -230,7 +179,6 @@ KernelParams base_params(sinet_ctx* c) {
     p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
     p.stream_groups = c->stream_groups;
     p.ranges_per_group = c->ranges_per_group;
-    p.stream_threads = c->stream_threads;
     p.pf_chunks = c->pf_chunks;
     p.range_counter = ws_u32(c, c->ws.counters);
     p.touched = ws_u32(c, c->ws.counters) + 4;
@@ -264,6 +212,7 @@ int do_materialize(sinet_ctx* c) {
 // span about the capture disorder; shuffled input spans the whole window.
 int probe_order(sinet_ctx* c, const sinet_records* r, int* out) {
     constexpr int kRuns = 64, kRun = 32;
+    // too small to judge: the stream kernel (exact for any order), decision not kept
     if (r->n < (uint64_t)kRuns * kRun) { *out = SINET_ORDER_STREAM; return SINET_OK; }
     std::vector<uint64_t> h((size_t)kRuns * kRun);
     for (int k = 0; k < kRuns; ++k) {
@@ -313,11 +262,17 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
     if (r->n == 0) return SINET_OK;
     int strategy = (int)c->cfg.order_hint;
     if (strategy == SINET_ORDER_AUTO) {
+        // probed once per histogram (sinet_reset forgets it) on the first batch large enough
+        // to judge; smaller batches take the stream kernel without deciding
         if (!c->auto_choice) {
-            int rc = probe_order(c, r, &c->auto_choice);
+            int choice = SINET_ORDER_STREAM;
+            int rc = probe_order(c, r, &choice);
             if (rc) return rc;
+            if (r->n >= 2048) c->auto_choice = choice;
+            strategy = choice;
+        } else {
+            strategy = c->auto_choice;
         }
-        strategy = c->auto_choice;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (strategy == SINET_ORDER_SHUFFLED) {
@@ -456,19 +411,11 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
     OPEN_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
     OPEN_CUDA(setup_hist_atomic());
     OPEN_CUDA(setup_hist_stream());
-    if (const char* a = std::getenv("SINET_AGG")) c->agg = std::atoi(a) != 0;
-    if (const char* g = std::getenv("SINET_STREAM_GROUPS")) c->stream_groups = (uint32_t)std::atoi(g);
-    if (const char* r = std::getenv("SINET_RANGES")) c->ranges_per_group = (uint32_t)std::atoi(r);
-    if (const char* t = std::getenv("SINET_STREAM_THREADS")) c->stream_threads = (uint32_t)std::atoi(t);
-    if (const char* x = std::getenv("SINET_EXCHANGE")) c->exchange = std::atoi(x);
-    if (const char* f = std::getenv("SINET_PF")) c->pf_chunks = (uint32_t)std::atoi(f);
-    if (const char* t = std::getenv("SINET_TAB")) c->tab_mode = std::atoi(t);
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
     OPEN_CUDA(cudaMemsetAsync(c->d_ws + c->ws.totals, 0, 16 * 8, c->stream));
     OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.cls2, c->table.cls2.data(), (size_t)kClsWords * 4, cudaMemcpyHostToDevice, c->stream));
-    OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.entry, c->table.entry.data(), 65536 * 4, cudaMemcpyHostToDevice, c->stream));
     if (c->nbnd)
         OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.bnd, c->table.bnd.data(), (size_t)c->nbnd * 4, cudaMemcpyHostToDevice, c->stream));
     OPEN_CUDA(cudaMemcpyAsync(c->d_ws + c->ws.rank, c->table.rank.data(), (size_t)kRankWords * 4, cudaMemcpyHostToDevice, c->stream));
@@ -508,11 +455,7 @@ void sinet_close(sinet_ctx* c) {
             if (c->kern_done[k]) cudaEventDestroy(c->kern_done[k]);
         }
         if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-        if (c->comm) {
-            std::string err;
-            NcclApi* api = nccl_api(&err);
-            if (api) api->CommDestroy(c->comm);
-        }
+        c->comm.reset();
     }
     delete c;
 }
@@ -530,6 +473,7 @@ int sinet_reset(sinet_ctx* c) {
     }
     c->reduced = false;
     c->materialized = false;
+    c->auto_choice = 0;
     return SINET_OK;
 }
 
@@ -645,51 +589,57 @@ int sinet_finalize(sinet_ctx* c) {
 int sinet_nccl_unique_id(void* out) {
     if (!out) return SINET_E_INVAL;
     std::string err;
-    NcclApi* api = nccl_api(&err);
-    if (!api) { std::fprintf(stderr, "sinet_nccl_unique_id: %s\n", err.c_str()); return SINET_E_NCCL; }
-    ncclUniqueId id;
-    if (api->GetUniqueId(&id) != 0) return SINET_E_NCCL;
-    std::memcpy(out, &id, sizeof id);
-    return SINET_OK;
+    int rc = nccl_unique_id(out, &err);
+    if (rc) std::fprintf(stderr, "sinet_nccl_unique_id: %s\n", err.c_str());
+    return rc;
 }
 
 int sinet_comm_init(sinet_ctx* c, const void* uid) {
     if (!c) return SINET_E_INVAL;
     if (!uid) return fail(c, SINET_E_INVAL, "NULL unique id");
     if (c->comm) return fail(c, SINET_E_STATE, "communicator already initialised");
-    NcclApi* api = nccl_api(&c->err);
-    if (!api) return SINET_E_NCCL;
     DeviceGuard dg(c->device);
-    ncclUniqueId id;
-    std::memcpy(&id, uid, sizeof id);
-    ncclResult_t r = api->CommInitRank(&c->comm, c->cfg.world, id, c->cfg.rank);
-    if (r != 0) { c->comm = nullptr; return fail(c, SINET_E_NCCL, std::string("ncclCommInitRank: ") + api->GetErrorString(r)); }
-    return SINET_OK;
+    c->comm = make_nccl_transport(c->cfg.world, c->cfg.rank, uid, &c->err);
+    return c->comm ? SINET_OK : SINET_E_NCCL;
 }
 
+int sinet_comm_init_hub(sinet_ctx* c, sinet_hub* hub) {
+    if (!c) return SINET_E_INVAL;
+    if (!hub) return fail(c, SINET_E_INVAL, "NULL hub");
+    if (c->comm) return fail(c, SINET_E_STATE, "communicator already initialised");
+    if (hub_world(hub) != c->cfg.world) return fail(c, SINET_E_INVAL, "hub world differs from cfg.world");
+    DeviceGuard dg(c->device);
+    c->comm = make_hub_transport(hub, c->cfg.rank, c->device, &c->err);
+    return c->comm ? SINET_OK : SINET_E_INVAL;
+}
+
+// Merge-scatter through the ctx's transport.  The same code runs over NCCL
+// (one process per GPU) and over the in-process hub (one thread per GPU).
 int sinet_reduce(sinet_ctx* c) {
     if (!c) return SINET_E_INVAL;
     if (c->reduced) return fail(c, SINET_E_STATE, "already reduced: call sinet_reset first");
     DeviceGuard dg(c->device);
-    const bool may_sparse = c->cfg.world > 1 && c->comm && c->exchange != 1 && c->ws.staging_bytes;
+    const int world = c->cfg.world, rank = c->cfg.rank;
+    const bool may_sparse = world > 1 && c->comm && c->exchange != 1 && c->ws.staging_bytes;
     if (!may_sparse) {
         int rc = do_materialize(c);
         if (rc) return rc;
     }
-    if (c->cfg.world > 1 || c->comm) {
-        if (!c->comm) return fail(c, SINET_E_NCCL, "no communicator: call sinet_comm_init");
-        NcclApi* api = nccl_api(&c->err);
-        if (!api) return SINET_E_NCCL;
-        const int world = c->cfg.world, rank = c->cfg.rank;
+    if (world > 1 || c->comm) {
+        if (!c->comm) return fail(c, SINET_E_NCCL, "no communicator: call sinet_comm_init or sinet_comm_init_hub");
+        Transport* T = c->comm.get();
+        const int tcode = std::strcmp(T->name(), "nccl") == 0 ? SINET_E_NCCL : SINET_E_CUDA;
         const size_t slice = (size_t)(c->geo.B_pad / (uint64_t)world) * 4u;   // u64 per rank
         unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.totals);
+        unsigned long long* xtot = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.xtotals);
         bool sparse = false;
         std::vector<Seg> sd, rv;
-        if (world > 1 && c->exchange != 1 && c->ws.staging_bytes) {
+        int rc = SINET_OK;
+        if (may_sparse) {
             // every rank's touched range, then the same plan (and decision) on every rank
             uint32_t* xr = ws_u32(c, c->ws.xranges);
-            ncclResult_t r = api->AllGather(ws_u32(c, c->ws.counters) + 4, xr, 2, kNcclUint32, c->comm, c->stream);
-            if (r != 0) return fail(c, SINET_E_NCCL, std::string("NCCL all-gather: ") + api->GetErrorString(r));
+            rc = T->all_gather_u32(ws_u32(c, c->ws.counters) + 4, xr, 2, c->stream, &c->err);
+            if (rc) return fail(c, rc == SINET_E_NCCL ? SINET_E_NCCL : tcode, "touched-range all-gather: " + c->err);
             std::vector<uint32_t> h((size_t)world * 2);
             SINET_CUDA(c, cudaMemcpyAsync(h.data(), xr, h.size() * 4, cudaMemcpyDeviceToHost, c->stream));
             SINET_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -722,27 +672,31 @@ int sinet_reduce(sinet_ctx* c) {
                 for (int o = 0; o < world && !mrc; ++o) mrc = mat(sd[o].first, sd[o].n);
                 if (mrc) return mrc;
             } else {
-                int rc = do_materialize(c);
-                if (rc) return rc;
+                int mrc = do_materialize(c);
+                if (mrc) return mrc;
             }
         }
-        ncclResult_t r = api->GroupStart();
-        if (sparse) {
+        rc = T->group_start(&c->err);
+        if (!rc && sparse) {
             // only the touched overlaps travel: send my partial bins inside each owner's range,
             // receive the other ranks' partial bins of my owned range into staging
             unsigned long long* stage = reinterpret_cast<unsigned long long*>(c->d_ws + c->ws.staging);
             size_t off = 0;
-            for (int o = 0; o < world && r == 0; ++o)
-                if (sd[o].n) r = api->Send(c->bins + sd[o].first * 4u, sd[o].n * 4u, kNcclUint64, o, c->comm, c->stream);
-            for (int q = 0; q < world && r == 0; ++q)
-                if (rv[q].n) { r = api->Recv(stage + off, rv[q].n * 4u, kNcclUint64, q, c->comm, c->stream); off += rv[q].n * 4u; }
-        } else {
-            r = api->ReduceScatter(c->bins, c->bins + slice * (size_t)rank, slice, kNcclUint64, kNcclSum, c->comm, c->stream);
+            for (int o = 0; o < world && !rc; ++o)
+                if (sd[o].n) rc = T->send_u64(c->bins + sd[o].first * 4u, sd[o].n * 4u, o, c->stream, &c->err);
+            for (int q = 0; q < world && !rc; ++q)
+                if (rv[q].n) { rc = T->recv_u64(stage + off, rv[q].n * 4u, q, c->stream, &c->err); off += rv[q].n * 4u; }
+        } else if (!rc) {
+            rc = T->reduce_scatter_u64(c->bins, c->bins + slice * (size_t)rank, slice, c->stream, &c->err);
+            if (!rc && std::strcmp(T->name(), "hub") == 0) c->launches++;   // k_sum_peers
         }
-        if (r == 0) r = api->AllReduce(tot, tot, 12, kNcclUint64, kNcclSum, c->comm, c->stream);
-        ncclResult_t r2 = api->GroupEnd();
-        if (r == 0) r = r2;
-        if (r != 0) return fail(c, SINET_E_NCCL, std::string("NCCL reduce: ") + api->GetErrorString(r));
+        if (!rc) {
+            rc = T->all_reduce_u64(tot, tot, 12, xtot, c->stream, &c->err);
+            if (!rc && std::strcmp(T->name(), "hub") == 0) c->launches++;
+        }
+        const int rc2 = T->group_end(c->stream, rc ? &c->err : &c->err);
+        if (!rc) rc = rc2;
+        if (rc) return fail(c, rc, std::string("merge (") + T->name() + "): " + c->err);
         if (sparse) {
             const unsigned long long* stage = reinterpret_cast<const unsigned long long*>(c->d_ws + c->ws.staging);
             size_t off = 0;
@@ -808,13 +762,25 @@ int sinet_read_bins(sinet_ctx* c, int dir, int metric, uint64_t first, uint64_t 
     return SINET_OK;
 }
 
+int sinet_rebin_frames(sinet_ctx* c, uint64_t factor, uint64_t* first_frame, uint64_t* n_frames) {
+    if (!c || factor == 0 || !first_frame || !n_frames) return c ? fail(c, SINET_E_INVAL, "rebin_frames: bad argument") : SINET_E_INVAL;
+    uint64_t lo, cnt;
+    sinet_owned_range(c, &lo, &cnt);
+    // frame k = absolute bins [k*factor, (k+1)*factor): the owned range meets frames
+    // floor(lo/f) .. ceil((lo+cnt)/f) - 1
+    *first_frame = lo / factor;
+    *n_frames = cnt ? (lo + cnt + factor - 1) / factor - lo / factor : 0;
+    return SINET_OK;
+}
+
 int sinet_rebin(sinet_ctx* c, uint64_t factor, uint64_t* d_out, uint64_t n_out) {
     if (!c) return SINET_E_INVAL;
     if (factor == 0 || !d_out || (reinterpret_cast<uintptr_t>(d_out) & 7u))
         return fail(c, SINET_E_INVAL, "rebin: factor must be >= 1 and d_out an 8-byte aligned device buffer");
-    uint64_t lo, cnt;
+    uint64_t lo, cnt, f0, nf;
     sinet_owned_range(c, &lo, &cnt);
-    if (n_out != (cnt + factor - 1) / factor) return fail(c, SINET_E_INVAL, "rebin: n_out must be ceil(owned bins / factor)");
+    sinet_rebin_frames(c, factor, &f0, &nf);
+    if (n_out != nf) return fail(c, SINET_E_INVAL, "rebin: n_out must be the frame count of sinet_rebin_frames");
     DeviceGuard dg(c->device);
     int rc = c->reduced ? SINET_OK : do_materialize(c);
     if (rc) return rc;
@@ -939,6 +905,21 @@ int sinet_set_tuning(sinet_ctx* c, int stream_groups, int warp_aggregation) {
         return fail(c, SINET_E_INVAL, "stream_groups must be 0, 1 or 2; warp_aggregation -1, 0 or 1");
     c->stream_groups = (uint32_t)stream_groups;
     if (warp_aggregation >= 0) c->agg = warp_aggregation != 0;
+    return SINET_OK;
+}
+
+int sinet_set_knob(sinet_ctx* c, const char* name, int64_t value) {
+    if (!c) return SINET_E_INVAL;
+    if (!name) return fail(c, SINET_E_INVAL, "NULL knob name");
+    const std::string k(name);
+    auto range = [&](int64_t lo, int64_t hi) { return value >= lo && value <= hi; };
+    if (k == "stream_groups" && range(0, 2)) c->stream_groups = (uint32_t)value;
+    else if (k == "warp_aggregation" && range(0, 1)) c->agg = value != 0;
+    else if (k == "ranges_per_group" && range(0, 64)) c->ranges_per_group = (uint32_t)value;
+    else if (k == "l2_prefetch_chunks" && range(0, 8)) c->pf_chunks = (uint32_t)value;
+    else if (k == "table_mode" && range(-1, 3)) c->tab_mode = (int)value;
+    else if (k == "exchange" && range(0, 2)) c->exchange = (int)value;
+    else return fail(c, SINET_E_INVAL, "unknown knob or value out of range: " + k);
     return SINET_OK;
 }
 

@@ -33,7 +33,4 @@ size_t sortreduce_scratch_bytes(uint64_t n, uint64_t nbins);
 cudaError_t launch_sortreduce(const KernelParams& p, void* scratch, size_t scratch_bytes, int sm_count,
                               cudaStream_t st, int* launches);
 
-cudaError_t launch_add_bins(unsigned long long* bins, const unsigned long long* in, uint64_t first, uint64_t n,
-                            int sm_count, cudaStream_t st);
-
 }  // namespace sinet

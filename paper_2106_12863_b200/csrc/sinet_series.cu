@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) k_rebin(const ulonglong2* __restrict__ bi
         for (int r = 0; r < kRun; ++r) {
             const uint64_t i = b0 + r;
             if (t < nthreads_needed && i < nb) {
-                const uint64_t k = i / factor;
+                const uint64_t k = (lo + i) / factor - lo / factor;   // absolute frame, from the first one met
                 if (key != ~0ull && k != key) {   // coarse boundary inside this thread's run
                     for (int m = 0; m < 4; ++m) if (v[m]) atomicAdd(out + key * 4 + m, v[m]);
                     v[0] = v[1] = v[2] = v[3] = 0ull;
@@ -149,23 +149,6 @@ __global__ void __launch_bounds__(256) k_sparse_write(const unsigned long long* 
         }
         __syncthreads();
     }
-}
-
-// Sparse multi-GPU exchange: owned bins [first, first+n) += received partial bins.
-__global__ void __launch_bounds__(256) k_add_bins(unsigned long long* bins, const unsigned long long* in,
-                                                  uint64_t first, uint64_t n) {
-    const uint64_t total = n * 4u;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)
-        bins[first * 4u + i] += in[i];
-}
-
-cudaError_t launch_add_bins(unsigned long long* bins, const unsigned long long* in, uint64_t first, uint64_t n,
-                            int sm_count, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
-    uint64_t blocks = (n * 4u + 255u) / 256u;
-    const uint64_t cap = (uint64_t)sm_count * 8u;
-    k_add_bins<<<(int)(blocks < cap ? blocks : cap), 256, 0, st>>>(bins, in, first, n);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_rebin(const unsigned long long* bins, uint64_t lo, uint64_t hi, uint64_t factor,

@@ -14,7 +14,7 @@ import torch
 from . import _native as N
 from ._native import check, lib
 
-__all__ = ["SinetHistogram", "shard_range", "owned_bin_range", "padded_bins"]
+__all__ = ["SinetHistogram", "SinetHub", "shard_range", "owned_bin_range", "padded_bins"]
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -40,6 +40,28 @@ def owned_bin_range(nbins: int, rank: int, world: int, tile_bins: int | None = N
 
 def _ptr(t: torch.Tensor | None):
     return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+class SinetHub:
+    """In-process rendezvous of `world` ranks (one host thread per GPU): ctxs that
+    join it merge through peer memory instead of NCCL (sinet_hub_create).  Keep it alive
+    while any joined SinetHistogram is open."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        check(lib.sinet_hub_create(ctypes.byref(h), int(world)), None, "hub_create")
+        self.handle, self.world = h, int(world)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.sinet_hub_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class SinetHistogram:
@@ -190,6 +212,12 @@ class SinetHistogram:
         dist.broadcast_object_list(obj, src=0, group=group)
         self.comm_init(obj[0])
 
+    def comm_init_hub(self, hub: "SinetHub"):
+        """Join an in-process hub (this ctx's rank/world must match it)."""
+        assert hub.world == self.world
+        check(lib.sinet_comm_init_hub(self.ctx, hub.handle), self.ctx, "comm_init_hub")
+        self._hub = hub   # keep the hub alive at least as long as this ctx
+
     def reduce(self):
         check(lib.sinet_reduce(self.ctx), self.ctx, "reduce")
 
@@ -229,13 +257,24 @@ class SinetHistogram:
               self.ctx, "read_bins")
         return out
 
+    def rebin_frames(self, factor: int):
+        """(first frame, number of frames) the owned range meets; frame F = bins [F*factor, (F+1)*factor)."""
+        f0, nf = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.sinet_rebin_frames(self.ctx, int(factor), ctypes.byref(f0), ctypes.byref(nf)), self.ctx,
+              "rebin_frames")
+        return f0.value, nf.value
+
     def rebin(self, factor: int) -> torch.Tensor:
-        """Coarser frames of the owned range: int64[n_out, 2 dir, 2 metric] on the device (NEXT-1)."""
-        lo, hi = self.owned_range()
-        n_out = (hi - lo + factor - 1) // factor
+        """Coarser frames (NEXT-1): int64[n_frames, 2 dir, 2 metric] on the device, entry k = the
+        owned bins of frame rebin_frames()[0] + k (frames aligned to the window start)."""
+        _, n_out = self.rebin_frames(factor)
         out = torch.empty((max(n_out, 1), 2, 2), dtype=torch.int64, device=self.device)
         check(lib.sinet_rebin(self.ctx, int(factor), _ptr(out), n_out), self.ctx, "rebin")
         return out[:n_out]
+
+    def set_knob(self, name: str, value: int):
+        """Named performance knob of the library (results identical for every value)."""
+        check(lib.sinet_set_knob(self.ctx, name.encode(), int(value)), self.ctx, "set_knob")
 
     def export_sparse(self, direction: int, capacity: int | None = None):
         """(bin start ms, count, bytes) of every nonzero-count bin of `direction`, ascending (NEXT-1)."""
@@ -317,7 +356,7 @@ def table_member_host(nets, lens, ips, labels=None) -> np.ndarray:
     return out
 
 
-def parse_text(text: torch.Tensor, tz_offset_min: int = 540, capacity: int | None = None,
+def parse_text(text: torch.Tensor, tz_offset_min: int = 0, capacity: int | None = None,
                status: bool = False, out: dict | None = None, workspace: torch.Tensor | None = None):
     """NEXT-3: PA-7080 session-log text (uint8 CUDA tensor, Table 1 lines) -> device columns.
 

@@ -327,7 +327,20 @@ def records(wl: Workload, lo: int = 0, hi: int | None = None, device="cpu", orde
     pos = torch.arange(lo, hi, dtype=torch.int64, device=device)
     if wl.order == "shuffled":
         pos = _feistel_perm(pos, wl.n, wl.seed)
-    i = order[pos]                     # draw index; every per-record draw is keyed by it
+    i = order[pos].to(torch.int64)     # draw index; every per-record draw is keyed by it
+    return _records_of_draws(wl, i)
+
+
+def draw_records(wl: Workload, lo: int, hi: int, device="cpu"):
+    """Records of draws [lo, hi) in draw order (no arrival sort).  Over [0, N) this is the
+    same multiset of records as ``records()`` in either order, so order-independent results
+    (the histogram) can be produced chunk by chunk without the global sort."""
+    assert 0 <= lo <= hi <= wl.n
+    return _records_of_draws(wl, torch.arange(lo, hi, dtype=torch.int64, device=torch.device(device)))
+
+
+def _records_of_draws(wl: Workload, i: torch.Tensor):
+    device = i.device
     ts = wl.window_start_ms + _ts_offsets(wl, i)
 
     # endpoint classes

@@ -46,7 +46,7 @@ def _worker(rank, world, port, out):
     cnt = merged[:2 * B].reshape(2, B)
     byt = merged[2 * B:4 * B].reshape(2, B)
     tot = merged[4 * B:]
-    olo, ohi = owned_bin_range(B, rank, world, tile_bins=512)
+    olo, ohi = owned_bin_range(B, rank, world)   # the library's tile (sinet_tile_bins)
     full = oracle.classify_histogram(*to_numpy(records(wl, order=order)), nets, lens, wl.window_start_ms,
                                      wl.window_ms, 1)
     ok = (np.array_equal(cnt[:, olo:ohi], full.count[:, olo:ohi]) and
@@ -105,7 +105,7 @@ def _sparse_worker(rank, world, port, out, order):
         f, n = send[o]
         if n:
             reqs.append(dist.isend(torch.from_numpy(mine[f:f + n].view(np.int64).copy()), dst=o))
-    olo, ohi = owned_bin_range(B, rank, world, tile_bins=256)
+    olo, ohi = owned_bin_range(B, rank, world)
     result = mine[olo:ohi].copy()
     for r in range(world):
         f, n = recv[r]

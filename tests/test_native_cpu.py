@@ -17,7 +17,19 @@ def test_every_header_symbol_is_exported():
     assert len(names) >= 20
     for name in names:
         assert hasattr(N.lib, name), f"libsinet.so does not export {name}"
-    assert N.lib.sinet_abi_version() == 1
+    assert N.lib.sinet_abi_version() == N._header_abi_version() == 2
+
+
+def test_hub_create_validates_world():
+    h = ctypes.c_void_p()
+    assert N.lib.sinet_hub_create(ctypes.byref(h), 0) == N.E_INVAL
+    assert N.lib.sinet_hub_create(ctypes.byref(h), 65) == N.E_INVAL
+    assert N.lib.sinet_hub_create(None, 2) == N.E_INVAL
+    assert N.lib.sinet_hub_create(ctypes.byref(h), 8) == N.OK and h.value
+    N.lib.sinet_hub_destroy(h)
+    N.lib.sinet_hub_destroy(None)
+    assert N.lib.sinet_comm_init_hub(None, None) == N.E_INVAL
+    assert N.lib.sinet_set_knob(None, b"stream_groups", 1) == N.E_INVAL
 
 
 def _cfg(**kw):

@@ -96,6 +96,41 @@ def test_member_table_order_insensitive(oracle_lib):
             a, [nets[i] for i in perm], [lens[i] for i in perm])
 
 
+def test_member_bylen_vs_bitstring_bruteforce(oracle_lib):
+    # the grouped-by-Z evaluation of the list (oracle_member_bylen_batch, used for the full-size
+    # C5 digests) against the 32-char bit-string brute force on 2 x 10^4 random (ip, list) cases
+    rnd = random.Random(4096)
+    for _ in range(20_000):
+        a, nets, lens = _random_case(rnd)
+        got = oracle_lib.member_bylen(np.array([a], np.uint32), nets, lens)[0]
+        assert got == brute.member_bitstring(a, nets, lens)
+
+
+def test_member_bylen_equals_linear_scan_on_c5_table(oracle_lib):
+    # C5's 4096-entry /8-/32 nested list: every interval edge +-1 and random addresses, both
+    # evaluations of Alg. 1 l.4-9 (linear scan, grouped by Z) agree address by address
+    nets, lens = prefix_table(WORKLOADS["c5"])
+    rng = np.random.default_rng(5)
+    ips = np.concatenate([edge_addresses(nets, lens), rng.integers(0, 1 << 32, 20_000, dtype=np.uint64).astype(np.uint32)])
+    got = oracle_lib.member_bylen(ips, nets, lens, threads=4)
+    want = np.array([oracle_lib.member(int(x), nets, lens) for x in ips], np.uint8)
+    np.testing.assert_array_equal(got, want)
+    assert 0 < int(got.sum()) < len(ips)
+
+
+def test_histogram_members_equals_classify(oracle_lib):
+    # memberships given per record, then the same post-discrimination steps: identical results
+    wl = WORKLOADS["c1"].with_(n=50_000)
+    nets, lens = prefix_table(wl)
+    ts, src, dst, nb = to_numpy(records(wl))[:4]
+    a = oracle_lib.classify_histogram(ts, src, dst, nb, nets, lens, wl.window_start_ms, wl.window_ms, 1)
+    b = oracle_lib.histogram_members(ts, oracle_lib.member_bylen(src, nets, lens), oracle_lib.member_bylen(dst, nets, lens),
+                                     nb, wl.window_start_ms, wl.window_ms, 1)
+    np.testing.assert_array_equal(a.count, b.count)
+    np.testing.assert_array_equal(a.bytes, b.bytes)
+    np.testing.assert_array_equal(a.totals, b.totals)
+
+
 # ----------------------------------------------------------------------------- worked fixture
 @pytest.mark.parametrize("case", ["src_priority_w1", "alg1_w1", "strict_w1", "src_priority_w5"])
 def test_f0_golden(oracle_lib, case):
