@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SINET_ABI_VERSION 2
+#define SINET_ABI_VERSION 3
 
 /* error codes */
 #define SINET_OK        0
@@ -261,6 +261,14 @@ int sinet_owned_range(sinet_ctx* ctx, uint64_t* first_bin, uint64_t* n_bins);
 int sinet_read_bins(sinet_ctx* ctx, int dir, int metric, uint64_t first_bin, uint64_t n_bins,
                     uint64_t* dst, int dst_is_device);
 
+/* Copy bins [first_bin, first_bin + n_bins) in the native layout, u64
+ * dst[n_bins][2 dir][2 metric] (32 bytes per bin: the paper's <timestamp,count>
+ * and <timestamp,bytes> of both directions), with ONE contiguous copy into
+ * dst (device if dst_is_device else host; page-locked host memory makes it an
+ * async DMA at full link rate; host copies synchronise the stream).  Errors:
+ * E_INVAL (NULL dst), E_RANGE (outside the owned range), E_CUDA. */
+int sinet_read_bins_raw(sinet_ctx* ctx, uint64_t first_bin, uint64_t n_bins, uint64_t* dst, int dst_is_device);
+
 /* NEXT-1, coarser frames: "Session data is grouped into one-hour frame bins"
  * (P:L323); "about 40,000 in 10 minutes".  Frame F = bins
  * [F*factor, (F+1)*factor) of the window (frames aligned to window_start).  The
@@ -372,9 +380,13 @@ int sinet_set_tuning(sinet_ctx* ctx, int stream_groups, int warp_aggregation);
 /* Named performance knobs (results are identical for every setting; they exist for A/B
  * measurements and tests): "stream_groups" 0..2, "warp_aggregation" 0/1,
  * "ranges_per_group" 0..64 (0 = default), "l2_prefetch_chunks" 0..8, "table_mode" -1..3
- * (as sinet_set_table_mode), "exchange" 0..2 (as sinet_set_exchange).
+ * (as sinet_set_table_mode), "exchange" 0..2 (as sinet_set_exchange), "stream_kernel" 0..2
+ * (0 automatic, 1 the group-barrier kernel k_hist_stream, 2 the warp-specialised k_hist_ws).
  * Errors: E_INVAL (unknown name or value out of range). */
 int sinet_set_knob(sinet_ctx* ctx, const char* name, int64_t value);
+/* Name of the dominant kernel the last classify call launched ("k_hist_ws",
+ * "k_hist_stream", "k_hist_atomic"; "" before the first call or for a NULL ctx). */
+const char* sinet_last_kernel(const sinet_ctx* ctx);
 /* Lookup-table encoding of the STREAM kernel (Alg. 1 l.6-9 compiled by sinet_open;
  * results are identical for every setting): -1 = automatic (the fastest that fits
  * in shared memory), 0 = byte /16 + /24 classes, 1 = packed 2-bit classes with

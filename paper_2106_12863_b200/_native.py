@@ -88,6 +88,7 @@ _SIGS = {
     "sinet_reduce": ([_vp], _i),
     "sinet_owned_range": ([_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i),
     "sinet_read_bins": ([_vp, _i, _i, _u64, _u64, _vp, _i], _i),
+    "sinet_read_bins_raw": ([_vp, _u64, _u64, _vp, _i], _i),
     "sinet_read_totals": ([_vp, ctypes.POINTER(Totals)], _i),
     "sinet_rebin": ([_vp, _u64, _vp, _u64], _i),
     "sinet_rebin_frames": ([_vp, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i),
@@ -103,6 +104,7 @@ _SIGS = {
     "sinet_set_kernel_timing": ([_vp, _i], _i),
     "sinet_kernel_time": ([_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)], _i),
     "sinet_last_strategy": ([_vp], _i),
+    "sinet_last_kernel": ([_vp], ctypes.c_char_p),
     "sinet_set_tuning": ([_vp, _i, _i], _i),
     "sinet_set_table_mode": ([_vp, _i], _i),
     "sinet_table_mode": ([_vp], _i),

@@ -103,9 +103,11 @@ struct sinet_ctx {
     bool reduced = false;
     bool materialized = false;
     int last_strategy = 0;
+    const char* last_kernel = "";   // dominant kernel of the last classify call
     int auto_choice = 0;          // strategy AUTO resolved by the first probe
     bool agg = false;             // warp aggregation of equal keys in the stream kernel (measured slower on C4)
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
+    uint32_t stream_kernel = 0;   // 0 auto, 1 k_hist_stream (group barriers), 2 k_hist_ws (warp-specialised)
     uint32_t ranges_per_group = 0;
     uint32_t pf_chunks = 0;           // L2 bulk prefetch distance (measured: off is fastest, C2 1.43 vs 1.46 ms)
     int tab_mode = -1;            // stream kernel lookup-table encoding: -1 automatic, 0..3 forced
@@ -178,6 +180,7 @@ KernelParams base_params(sinet_ctx* c) {
     p.nbnd = c->nbnd;
     p.small = table_small(c->nbnd, c->table.n_mixed) ? 1u : 0u;
     p.stream_groups = c->stream_groups;
+    p.stream_kernel = c->stream_kernel;
     p.ranges_per_group = c->ranges_per_group;
     p.pf_chunks = c->pf_chunks;
     p.range_counter = ws_u32(c, c->ws.counters);
@@ -255,6 +258,8 @@ int prepare_params(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags, Kernel
     return SINET_OK;
 }
 
+constexpr bool kWsAuto = false;   // k_hist_ws opt-in (knob stream_kernel=2) until measured on the GPU
+
 int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
     KernelParams p;
     int prc = prepare_params(c, r, d_tags, &p);
@@ -287,9 +292,21 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
     }
     if (strategy == SINET_ORDER_SHUFFLED) {
         SINET_CUDA(c, launch_hist_atomic(p, c->atomic_grid, c->stream));
+        c->last_kernel = "k_hist_atomic";
     } else {
         // time-window privatisation, write-once bins; untouched tiles stay virtual
-        SINET_CUDA(c, launch_hist_stream(p, c->sm_count, c->agg, c->stream));
+        // k_hist_ws for dense input (>= 1 record per bin: its 15 workers' in-flight chunks stay
+        // inside the ring), k_hist_stream (8192-bin ring per 512 threads) for sparse input
+        const int tab = stream_table_mode(p.has_bytes != 0u, p.nbnd, p.n_mixed, p.tab_mode);
+        const bool ws = p.stream_kernel == 2u ||
+                        (kWsAuto && p.stream_kernel == 0u && p.n >= (uint64_t)p.nbins && hist_ws_fits(tab, p.nbnd, p.n_mixed));
+        if (ws && hist_ws_fits(tab, p.nbnd, p.n_mixed)) {
+            SINET_CUDA(c, launch_hist_ws(p, c->sm_count, c->stream));
+            c->last_kernel = "k_hist_ws";
+        } else {
+            SINET_CUDA(c, launch_hist_stream(p, c->sm_count, c->agg, c->stream));
+            c->last_kernel = "k_hist_stream";
+        }
         c->materialized = false;
     }
     c->launches++;
@@ -344,6 +361,8 @@ int sinet_exchange_plan(int32_t world, int32_t rank, uint64_t nbins, uint64_t nb
 }
 
 int sinet_abi_version(void) { return SINET_ABI_VERSION; }
+
+const char* sinet_last_kernel(const sinet_ctx* c) { return c ? c->last_kernel : ""; }
 uint32_t sinet_tile_bins(void) { return kTileBins; }
 uint32_t sinet_parse_chunk_bytes(void) { return kParseChunk; }
 
@@ -411,6 +430,7 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
     OPEN_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
     OPEN_CUDA(setup_hist_atomic());
     OPEN_CUDA(setup_hist_stream());
+    OPEN_CUDA(setup_hist_ws());
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
@@ -762,6 +782,22 @@ int sinet_read_bins(sinet_ctx* c, int dir, int metric, uint64_t first, uint64_t 
     return SINET_OK;
 }
 
+int sinet_read_bins_raw(sinet_ctx* c, uint64_t first, uint64_t n, uint64_t* dst, int dst_is_device) {
+    if (!c) return SINET_E_INVAL;
+    uint64_t lo, cnt;
+    sinet_owned_range(c, &lo, &cnt);
+    if (first < lo || first > lo + cnt || n > lo + cnt - first) return fail(c, SINET_E_RANGE, "bin range outside the owned range");
+    if (n == 0) return SINET_OK;
+    if (!dst) return fail(c, SINET_E_INVAL, "NULL destination");
+    DeviceGuard dg(c->device);
+    int rc = c->reduced ? SINET_OK : do_materialize(c);
+    if (rc) return rc;
+    SINET_CUDA(c, cudaMemcpyAsync(dst, c->bins + first * 4u, n * 32u,
+                                  dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    if (!dst_is_device) SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SINET_OK;
+}
+
 int sinet_rebin_frames(sinet_ctx* c, uint64_t factor, uint64_t* first_frame, uint64_t* n_frames) {
     if (!c || factor == 0 || !first_frame || !n_frames) return c ? fail(c, SINET_E_INVAL, "rebin_frames: bad argument") : SINET_E_INVAL;
     uint64_t lo, cnt;
@@ -915,6 +951,7 @@ int sinet_set_knob(sinet_ctx* c, const char* name, int64_t value) {
     auto range = [&](int64_t lo, int64_t hi) { return value >= lo && value <= hi; };
     if (k == "stream_groups" && range(0, 2)) c->stream_groups = (uint32_t)value;
     else if (k == "warp_aggregation" && range(0, 1)) c->agg = value != 0;
+    else if (k == "stream_kernel" && range(0, 2)) c->stream_kernel = (uint32_t)value;
     else if (k == "ranges_per_group" && range(0, 64)) c->ranges_per_group = (uint32_t)value;
     else if (k == "l2_prefetch_chunks" && range(0, 8)) c->pf_chunks = (uint32_t)value;
     else if (k == "table_mode" && range(-1, 3)) c->tab_mode = (int)value;

@@ -18,6 +18,9 @@ int hist_atomic_blocks_per_sm(const KernelParams& p);
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st);
 
 cudaError_t setup_hist_stream();
+cudaError_t setup_hist_ws();
+cudaError_t launch_hist_ws(const KernelParams& p, int sm_count, cudaStream_t st);
+bool hist_ws_fits(int tab, uint32_t nbnd, uint32_t n_mixed);
 cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cudaStream_t st);
 constexpr uint32_t kStreamWindowBins = 4096;   // smallest ring of the stream kernel (AUTO probe threshold)
 

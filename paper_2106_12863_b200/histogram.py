@@ -257,6 +257,19 @@ class SinetHistogram:
               self.ctx, "read_bins")
         return out
 
+    def read_bins_raw(self, out: torch.Tensor | None = None, first: int | None = None, n: int | None = None):
+        """Owned bins [first, first + n) in the native layout, int64[n, 2 dir, 2 metric], copied with one
+        sinet_read_bins_raw call into `out` (a device tensor, or a host tensor -- pinned for full speed)."""
+        lo, hi = self.owned_range()
+        first = lo if first is None else int(first)
+        n = hi - first if n is None else int(n)
+        if out is None:
+            out = torch.empty((n, 2, 2), dtype=torch.int64)
+        assert out.dtype == torch.int64 and out.is_contiguous() and out.numel() >= 4 * n
+        dev = out.device.type == "cuda"
+        check(lib.sinet_read_bins_raw(self.ctx, first, n, _ptr(out), 1 if dev else 0), self.ctx, "read_bins_raw")
+        return out
+
     def rebin_frames(self, factor: int):
         """(first frame, number of frames) the owned range meets; frame F = bins [F*factor, (F+1)*factor)."""
         f0, nf = ctypes.c_uint64(), ctypes.c_uint64()
@@ -308,6 +321,10 @@ class SinetHistogram:
     @property
     def last_strategy(self) -> int:
         return int(lib.sinet_last_strategy(self.ctx))
+
+    @property
+    def last_kernel(self) -> str:
+        return lib.sinet_last_kernel(self.ctx).decode()
 
     def set_tuning(self, stream_groups: int = 0, warp_aggregation: int = -1):
         """Stream-kernel layout (0 auto / 1 / 2 groups) and warp aggregation (1/0, -1 unchanged)."""

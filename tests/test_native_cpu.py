@@ -17,7 +17,7 @@ def test_every_header_symbol_is_exported():
     assert len(names) >= 20
     for name in names:
         assert hasattr(N.lib, name), f"libsinet.so does not export {name}"
-    assert N.lib.sinet_abi_version() == N._header_abi_version() == 2
+    assert N.lib.sinet_abi_version() == N._header_abi_version() == 3
 
 
 def test_hub_create_validates_world():

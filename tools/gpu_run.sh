@@ -1,0 +1,32 @@
+#!/bin/bash
+# One parameterised GPU job for gpurun:  gpurun -- bash tools/gpu_run.sh TAG STEP [STEP ...]
+# Steps: smoke pytest pytest_merge bench ref c1 c3 c4 c5 shuf launches ncu_c2 ncu_c4 ncu_c5 san digests
+# Every output lands in gpurun_out/TAG_<step>.txt (merged back by gpurun).
+set -x
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+TAG=$1; shift
+O=gpurun_out/${TAG}
+python -c "import paper_2106_12863_b200" || exit 1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > ${O}_gpu.txt 2>&1
+lscpu > ${O}_lscpu.txt 2>&1
+B="timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse"
+for s in "$@"; do
+  case $s in
+    smoke) timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > ${O}_smoke.txt 2>&1 ;;
+    pytest) timeout 2400 python -m pytest tests -m gpu -q -x --timeout 1200 > ${O}_pytest_gpu.txt 2>&1 ;;
+    pytest_merge) timeout 1200 python -m pytest tests/test_gpu_merge.py -m gpu -q -x --timeout 900 > ${O}_pytest_merge.txt 2>&1 ;;
+    bench) timeout 1200 python bench.py > ${O}_bench.txt 2>&1 ;;
+    ref) timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > ${O}_ref.txt 2>&1 ;;
+    c1|c2|c3|c4|c5) $B --config $s > ${O}_$s.txt 2>&1 ;;
+    shuf) $B --order shuffled > ${O}_shuf.txt 2>&1 ;;
+    shuf_c4) $B --config c4 --order shuffled > ${O}_shuf_c4.txt 2>&1 ;;
+    launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_run.txt 2>&1 ;;
+    ncu_c2) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c2 python bench.py --steps 2 --warmup 1 --profile > ${O}_ncu_c2_run.txt 2>&1 ;;
+    ncu_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile > ${O}_ncu_c4_run.txt 2>&1 ;;
+    ncu_c5) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c5 python bench.py --config c5 --steps 2 --warmup 1 --profile > ${O}_ncu_c5_run.txt 2>&1 ;;
+    san) for t in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $t python tools/sanitize_case.py > ${O}_san_$t.txt 2>&1; done ;;
+    digests) timeout 2400 python tools/oracle_digests.py --check-gpu > ${O}_digests.txt 2>&1 ;;
+    *) echo "unknown step $s" ;;
+  esac
+done
+tail -n 3 ${O}_*.txt | cut -c1-400
