@@ -405,6 +405,9 @@ def open_hist(wl, cx, stream):
     for kv in cx.args.knob:
         name, _, val = kv.partition("=")
         h.set_knob(name, int(val))
+    if wl.order == "shuffled":
+        # partition-then-bin scratch for the whole shard (one sub-batch: every bin written once)
+        h.set_scratch(S.shard_range(wl.n, cx.rank, cx.world)[1] - S.shard_range(wl.n, cx.rank, cx.world)[0])
     return h, nets, lens
 
 

@@ -181,6 +181,19 @@ size_t sinet_sortreduce_scratch_bytes(const sinet_config* cfg, uint64_t n);
 int sinet_classify_histogram_sortreduce(sinet_ctx* ctx, const sinet_records* recs,
                                         void* d_scratch, size_t scratch_bytes);
 
+/* Unordered input, partition then bin (SURVEY §8(d) strategy S4; the paper's tiling of a
+ * problem that "does not fit in the cache", §4): with a caller scratch buffer
+ * registered here, batches the order probe finds unordered (or cfg.order_hint SHUFFLED) are
+ * radix-partitioned by time into buckets of 8192 ms bins and every bucket is reduced in
+ * shared memory and written once, in sub-batches of as many records as the scratch holds
+ * (24 B/record + ~0.3 MB).  Without scratch such batches take the L2-atomic kernel.  Same
+ * result either way.  Windows of at most 2^27 bins.  sinet_partition_scratch_bytes(cfg, m)
+ * = bytes for sub-batches of m >= 2^16 records (0 if unsupported).  set_scratch: 256-byte
+ * aligned device buffer the library may use until it is replaced or removed (NULL / 0
+ * removes it); it must not be used by anything else meanwhile.  Errors: E_INVAL, E_ALIGN. */
+size_t sinet_partition_scratch_bytes(const sinet_config* cfg, uint64_t max_records);
+int sinet_set_scratch(sinet_ctx* ctx, void* d_scratch, size_t bytes);
+
 /* NEXT-2, watchlist filter (Figs 8-11: 300 AbuseIPDB addresses P:L345-350, 877
  * GRIZZLY STEPPE addresses P:L366-370): from now on only records whose source OR
  * destination equals a listed address are counted (totals and bins; tags still
@@ -381,7 +394,8 @@ int sinet_set_tuning(sinet_ctx* ctx, int stream_groups, int warp_aggregation);
  * measurements and tests): "stream_groups" 0..2, "warp_aggregation" 0/1,
  * "ranges_per_group" 0..64 (0 = default), "l2_prefetch_chunks" 0..8, "table_mode" -1..3
  * (as sinet_set_table_mode), "exchange" 0..2 (as sinet_set_exchange), "stream_kernel" 0..2
- * (0 automatic, 1 the group-barrier kernel k_hist_stream, 2 the warp-specialised k_hist_ws).
+ * (0 automatic, 1 the group-barrier kernel k_hist_stream, 2 the warp-specialised k_hist_ws),
+ * "shuffled_kernel" 0..1 (0 partition-then-bin when scratch is registered, 1 L2 atomics).
  * Errors: E_INVAL (unknown name or value out of range). */
 int sinet_set_knob(sinet_ctx* ctx, const char* name, int64_t value);
 /* Name of the dominant kernel the last classify call launched ("k_hist_ws",

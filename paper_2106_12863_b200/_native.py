@@ -97,6 +97,8 @@ _SIGS = {
     "sinet_comm_init_hub": ([_vp, _vp], _i),
     "sinet_set_knob": ([_vp, ctypes.c_char_p, ctypes.c_int64], _i),
     "sinet_sortreduce_scratch_bytes": ([_CP, _u64], ctypes.c_size_t),
+    "sinet_partition_scratch_bytes": ([_CP, _u64], ctypes.c_size_t),
+    "sinet_set_scratch": ([_vp, _vp, ctypes.c_size_t], _i),
     "sinet_classify_histogram_sortreduce": ([_vp, ctypes.POINTER(Records), _vp, ctypes.c_size_t], _i),
     "sinet_export_sparse": ([_vp, _i, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i),
     "sinet_last_error": ([_vp], ctypes.c_char_p),

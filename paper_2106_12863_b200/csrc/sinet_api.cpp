@@ -108,6 +108,10 @@ struct sinet_ctx {
     bool agg = false;             // warp aggregation of equal keys in the stream kernel (measured slower on C4)
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t stream_kernel = 0;   // 0 auto, 1 k_hist_stream (group barriers), 2 k_hist_ws (warp-specialised)
+    uint32_t shuffled_kernel = 0; // 0 auto (partition-then-bin when scratch is set), 1 L2 atomics only
+    void* scratch = nullptr;      // caller scratch for the partitioned path (sinet_set_scratch)
+    size_t scratch_bytes = 0;
+    uint64_t scratch_cap = 0;     // records per partitioned sub-batch
     uint32_t ranges_per_group = 0;
     uint32_t pf_chunks = 0;           // L2 bulk prefetch distance (measured: off is fastest, C2 1.43 vs 1.46 ms)
     int tab_mode = -1;            // stream kernel lookup-table encoding: -1 automatic, 0..3 forced
@@ -258,6 +262,7 @@ int prepare_params(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags, Kernel
     return SINET_OK;
 }
 
+constexpr uint64_t kPartMinCap = 1u << 16;   // records: smaller scratch is not worth the passes
 constexpr bool kWsAuto = false;   // k_hist_ws opt-in (knob stream_kernel=2) until measured on the GPU
 
 int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
@@ -280,7 +285,9 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
         }
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (strategy == SINET_ORDER_SHUFFLED) {
+    const bool partitioned = strategy == SINET_ORDER_SHUFFLED && c->scratch_cap >= kPartMinCap &&
+                             c->shuffled_kernel == 0u && partition_supported((uint32_t)c->geo.B);
+    if (strategy == SINET_ORDER_SHUFFLED && !partitioned) {
         // materialise every tile, then L2 atomics (any order)
         int rc = do_materialize(c);
         if (rc) return rc;
@@ -290,7 +297,25 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
         SINET_CUDA(c, cudaEventCreate(&e1));
         SINET_CUDA(c, cudaEventRecord(e0, c->stream));
     }
-    if (strategy == SINET_ORDER_SHUFFLED) {
+    uint64_t n_launched = 1;
+    if (partitioned) {
+        n_launched = 0;
+        // sub-batches of scratch_cap records (a multiple of 4: every sub-batch keeps the batch's
+        // 16-byte phase); tiles are claimed per sub-batch, so later ones add onto earlier ones
+        const PartLayout L = part_layout(c->scratch_cap, (uint32_t)c->geo.B);
+        for (uint64_t o = 0; o < r->n; o += c->scratch_cap) {
+            const uint64_t m = (r->n - o < c->scratch_cap) ? r->n - o : c->scratch_cap;
+            sinet_records sub{r->ts_ms + o, r->src + o, r->dst + o, r->bytes + o, m};
+            KernelParams q;
+            int prc2 = prepare_params(c, &sub, d_tags ? d_tags + o : nullptr, &q);
+            if (prc2) return prc2;
+            int k = 0;
+            SINET_CUDA(c, launch_partitioned(q, c->scratch, L, c->sm_count, c->stream, &k));
+            n_launched += (uint64_t)k;
+        }
+        c->materialized = false;
+        c->last_kernel = "k_part (count, scatter, fine, bin)";
+    } else if (strategy == SINET_ORDER_SHUFFLED) {
         SINET_CUDA(c, launch_hist_atomic(p, c->atomic_grid, c->stream));
         c->last_kernel = "k_hist_atomic";
     } else {
@@ -309,7 +334,7 @@ int classify_device(sinet_ctx* c, const sinet_records* r, uint8_t* d_tags) {
         }
         c->materialized = false;
     }
-    c->launches++;
+    c->launches += n_launched;
     c->last_strategy = strategy;
     if (c->timing) {
         SINET_CUDA(c, cudaEventRecord(e1, c->stream));
@@ -431,6 +456,7 @@ int sinet_open_labelled(sinet_ctx** out, const sinet_config* cfg, const uint32_t
     OPEN_CUDA(setup_hist_atomic());
     OPEN_CUDA(setup_hist_stream());
     OPEN_CUDA(setup_hist_ws());
+    OPEN_CUDA(setup_partition());
     c->atomic_grid = c->sm_count * hist_atomic_blocks_per_sm(base_params(c));
     c->materialize_grid = c->sm_count * 8;
     // upload the compiled table; zero totals and tile states
@@ -536,6 +562,33 @@ int sinet_classify_histogram_host(sinet_ctx* c, const sinet_records* h, void* d_
         SINET_CUDA(c, cudaEventRecord(c->kern_done[b], c->stream));
     }
     SINET_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SINET_OK;
+}
+
+size_t sinet_partition_scratch_bytes(const sinet_config* cfg, uint64_t max_records) {
+    std::string err;
+    Geometry g;
+    if (!check_cfg(cfg, &err, &g) || !partition_supported((uint32_t)g.B) || max_records < kPartMinCap) return 0;
+    return part_layout((max_records + 3) & ~3ull, (uint32_t)g.B).total;
+}
+
+int sinet_set_scratch(sinet_ctx* c, void* d_scratch, size_t bytes) {
+    if (!c) return SINET_E_INVAL;
+    if (!d_scratch || bytes == 0) { c->scratch = nullptr; c->scratch_bytes = 0; c->scratch_cap = 0; return SINET_OK; }
+    if (reinterpret_cast<uintptr_t>(d_scratch) & 255u) return fail(c, SINET_E_ALIGN, "scratch must be 256-byte aligned");
+    if (!partition_supported((uint32_t)c->geo.B)) return fail(c, SINET_E_INVAL, "partitioned path: window of more than 2^27 bins");
+    // the largest multiple of 4 records (< 2^31: u32 offsets) whose layout fits
+    uint64_t lo = 0, hi = (bytes / 24u + 4u) & ~3ull;
+    if (hi >= (1ull << 31)) hi = (1ull << 31) - 4u;
+    while (lo < hi) {
+        const uint64_t mid = ((lo + hi) / 2 + 4u) & ~3ull;
+        if (mid > hi) break;
+        if (part_layout(mid, (uint32_t)c->geo.B).total <= bytes) lo = mid; else hi = mid - 4u;
+    }
+    if (lo < kPartMinCap) return fail(c, SINET_E_INVAL, "scratch smaller than sinet_partition_scratch_bytes(cfg, 2^16)");
+    c->scratch = d_scratch;
+    c->scratch_bytes = bytes;
+    c->scratch_cap = lo;
     return SINET_OK;
 }
 
@@ -952,6 +1005,7 @@ int sinet_set_knob(sinet_ctx* c, const char* name, int64_t value) {
     if (k == "stream_groups" && range(0, 2)) c->stream_groups = (uint32_t)value;
     else if (k == "warp_aggregation" && range(0, 1)) c->agg = value != 0;
     else if (k == "stream_kernel" && range(0, 2)) c->stream_kernel = (uint32_t)value;
+    else if (k == "shuffled_kernel" && range(0, 1)) c->shuffled_kernel = (uint32_t)value;
     else if (k == "ranges_per_group" && range(0, 64)) c->ranges_per_group = (uint32_t)value;
     else if (k == "l2_prefetch_chunks" && range(0, 8)) c->pf_chunks = (uint32_t)value;
     else if (k == "table_mode" && range(-1, 3)) c->tab_mode = (int)value;

@@ -32,6 +32,21 @@ cudaError_t launch_sparse(const unsigned long long* bins, uint64_t lo, uint64_t 
                           unsigned long long* o_cnt, unsigned long long* o_bytes, uint64_t capacity,
                           cudaStream_t st);
 
+// unordered input: partition by time, then bin (sinet_partition.cu)
+constexpr uint32_t kMaxFine = 16384;     // fine buckets of 8192 bins: windows of up to 2^27 bins
+constexpr uint32_t kMaxCoarse = 128;
+struct PartLayout {
+    uint64_t cap;                        // records per sub-batch
+    uint32_t nf, nc;                     // fine / coarse buckets of the window
+    size_t by_a, by_b, key_a, key_b, fine_cnt, fine_base, fine_cur, unit_base, coarse_base, coarse_cur,
+        cunit_base, counters, total;     // byte offsets in the scratch buffer, total size
+};
+PartLayout part_layout(uint64_t cap, uint32_t nbins);
+bool partition_supported(uint32_t nbins);
+cudaError_t setup_partition();
+cudaError_t launch_partitioned(const KernelParams& p, void* scratch, const PartLayout& L, int sm_count,
+                               cudaStream_t st, int* launches);
+
 size_t sortreduce_scratch_bytes(uint64_t n, uint64_t nbins);
 cudaError_t launch_sortreduce(const KernelParams& p, void* scratch, size_t scratch_bytes, int sm_count,
                               cudaStream_t st, int* launches);

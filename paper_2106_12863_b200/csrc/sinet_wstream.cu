@@ -16,10 +16,10 @@
 //     the high word to HBM).  A record outside the resident tiles [lo, top) -- later
 //     than the history kept or ahead of the window -- goes to HBM through the tile
 //     protocol (sinet_tiles.cuh).  After each chunk a worker publishes its newest tile
-//     and a chunk sequence number; that is all the coordination it does.
+//     and the `lo` that chunk ran with; that is all the coordination it does.
 //   * 1 MANAGER warp slides the window: once every worker's newest tile is kHist tiles
 //     past a tile, it raises `lo` (workers see it at their next chunk), waits until every
-//     worker has started a chunk after that (a sequence-number handshake, polled), then
+//     worker has finished a chunk that ran with the new `lo` (polled, no fences), then
 //     retires the tiles: claims them (one CAS per tile, all in flight at once), converts
 //     each ring tile to the bins' u64 layout in a staging buffer, and hands it to the TMA
 //     engine -- `cp.async.bulk` (a bulk store) for a tile it won, `cp.reduce.async.bulk
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
     uint32_t* s_win = smem;                                                    // cnt[WS][2] | lo[WS][2]
     unsigned long long* s_stage = reinterpret_cast<unsigned long long*>(smem + WS * 4u);   // 2 x u64[256][4]
     uint32_t* s_tab = smem + WS * 4u + 2u * kStageBytes / 4u;
-    __shared__ uint32_t s_head[kWorkers], s_seq[kWorkers], s_done[kWorkers], s_min[kWorkers], s_max[kWorkers];
+    // per worker: newest tile (a hint), the `lo` its last finished chunk ran with, done flag
+    __shared__ uint32_t s_head[kWorkers], s_used[kWorkers], s_done[kWorkers], s_min[kWorkers], s_max[kWorkers];
     __shared__ uint32_t s_lo, s_top, s_next;
     __shared__ uint32_t s_range;
     __shared__ unsigned long long s_tot[16 * 12];
@@ -107,7 +108,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
     const bool manager = warp == kWorkers;
     for (uint32_t i = threadIdx.x; i < WS; i += kWsThreads) reinterpret_cast<uint4*>(s_win)[i] = make_uint4(0u, 0u, 0u, 0u);
     const auto T = stage_stream_table<kTab>(p, s_tab);
-    if (threadIdx.x < kWorkers) s_seq[threadIdx.x] = 0u;
     __syncthreads();
 
     const uint32_t prev_word = p.epoch > 1 ? (((p.epoch - 1u) << 2) | kTileInit) : 0u;
@@ -122,7 +122,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
     WarpTotals tot;
     tot.zero();
     uint32_t gmin = 0xFFFFFFFFu, gmax = 0u;   // extent of this warp's binned records
-    uint32_t seq = 0u;                        // worker: chunks finished (published in s_seq)
     uint32_t nstage = 0u;                     // manager: bulk operations issued (staging buffer parity)
 
     for (;;) {   // record ranges handed out dynamically (one atomic per range)
@@ -167,7 +166,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                 lo0 = (tmax >= tmin + (NT - 2u)) ? tmax - (NT - 2u) : tmin;
             }
             if (lane == 0) { s_lo = lo0; s_top = lo0 + NT; }
-            if (lane < kWorkers) { s_head[lane] = lo0; s_done[lane] = 0u; }   // tiles (s_max holds bins)
+            if (lane < kWorkers) { s_head[lane] = lo0; s_done[lane] = 0u; s_used[lane] = 0u; }   // tiles (s_max: bins)
         }
         __syncthreads();
 
@@ -291,15 +290,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                                        out ? byt : ((uint64_t)hv << 32));
                     }
                 }
-                // ---- publish progress: newest tile, chunk sequence number (release: this
-                // warp's ring atomics happen before it); then see the manager's window
+                // ---- publish progress: the newest tile (a hint for the manager) and the `lo` this
+                // chunk ran with (release: the warp's ring atomics happen before it).  Once a
+                // worker has published lo' >= L, none of its chunks touches a tile below L again:
+                // earlier chunks are finished, and later ones read lo >= lo' (read-read coherence).
                 bmax = __reduce_max_sync(kFull, bmax);
                 head = max(head, bmax / kTileBins);
                 __syncwarp();
                 if (lane == 0) {
                     *reinterpret_cast<volatile uint32_t*>(&s_head[warp]) = head;
-                    sts_release(&s_seq[warp], ++seq);
-                    __threadfence_block();   // Dekker with the manager's lo store + seq snapshot
+                    sts_release(&s_used[warp], lo);
                 }
                 k = kn;
                 cur = nxt;
@@ -311,13 +311,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                 }
             }
             __syncwarp();
-            if (lane == 0) {
-                sts_release(&s_seq[warp], ++seq);
-                sts_release(&s_done[warp], 1u);   // s_head keeps this warp's final newest tile
-            }
+            if (lane == 0) sts_release(&s_done[warp], 1u);   // s_head keeps this warp's final newest tile
         } else {
             // ================================================================ manager
-            uint32_t lo = s_lo, raised = lo, hull_hi = lo, snap = 0u;
+            uint32_t lo = s_lo, raised = lo, hull_hi = lo;
             bool hs = false;              // a raise of lo awaits the workers' handshake
             unsigned pub_m = 0u;          // won tiles of the last batch, published after their bulk stores
             uint32_t pub_base = 0u;
@@ -403,12 +400,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
             for (;;) {
                 publish();
                 const bool dn = (lane < kWorkers) ? lds_acquire(&s_done[lane]) != 0u : true;
-                const uint32_t sq = (lane < kWorkers) ? lds_acquire(&s_seq[lane]) : 0u;
+                const uint32_t used = (lane < kWorkers) ? lds_acquire(&s_used[lane]) : 0u;
                 const uint32_t hd = (lane < kWorkers) ? lds_volatile(&s_head[lane]) : 0u;
                 const bool all_done = __all_sync(kFull, dn);
                 const uint32_t hmin = __reduce_min_sync(kFull, dn ? kDone : hd);   // finished workers do not pin the window
                 hull_hi = max(hull_hi, __reduce_max_sync(kFull, hd));
-                if (hs && __all_sync(kFull, dn || sq != snap)) {
+                if (hs && __all_sync(kFull, dn || used >= raised)) {
                     __syncwarp();   // every lane's ring reads after the workers' releases (acquired above)
                     retire(lo, raised);
                     lo = raised;
@@ -420,10 +417,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                     if (all_done) target = min(lo + NT, hull_hi + 1u);
                     else if (hmin >= lo + kHist + kBatch) target = min(lo + NT, hmin - kHist);
                     if (target > lo) {
-                        if (lane == 0) { sts_release(&s_lo, target); __threadfence_block(); }
-                        __syncwarp();
-                        __threadfence_block();   // Dekker: lo store before every lane's seq snapshot
-                        snap = (lane < kWorkers) ? lds_acquire(&s_seq[lane]) : 0u;
+                        if (lane == 0) sts_release(&s_lo, target);
                         raised = target;
                         hs = true;
                         continue;

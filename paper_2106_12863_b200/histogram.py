@@ -177,6 +177,21 @@ class SinetHistogram:
               self.ctx, "classify_sortreduce")
         return scratch
 
+    def set_scratch(self, max_records: int | None = 1 << 27):
+        """Register device scratch for unordered batches (partition then bin, sub-batches of
+        `max_records`; ~24 B/record).  None removes it (unordered batches then take L2 atomics)."""
+        if max_records is None:
+            check(lib.sinet_set_scratch(self.ctx, None, 0), self.ctx, "set_scratch")
+            self._scratch = None
+            return
+        need = lib.sinet_partition_scratch_bytes(ctypes.byref(self.cfg), int(max_records))
+        if need == 0:
+            raise N.SinetError(N.E_INVAL, "partitioned path unsupported for this window (> 2^27 bins) or size")
+        self._scratch = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
+        off = (-self._scratch.data_ptr()) % 256
+        check(lib.sinet_set_scratch(self.ctx, ctypes.c_void_p(self._scratch.data_ptr() + off), need), self.ctx,
+              "set_scratch")
+
     def set_watchlist(self, ips):
         """NEXT-2: count only records with a listed source or destination (None/[] removes it)."""
         ips = np.ascontiguousarray(np.asarray([] if ips is None else ips, dtype=np.uint32))

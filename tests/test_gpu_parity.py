@@ -34,7 +34,7 @@ def dev_cols(cols, device="cuda"):
 
 
 def gpu_run(S, nets, lens, cols, start, window, width=1, lut=LUT_SRC_PRIORITY, order=0, chunks=None,
-            tags=False, groups=0, agg=-1, tab=-1):
+            tags=False, groups=0, agg=-1, tab=-1, scratch=None):
     """groups: 0 automatic kernel/layout, 1 / 2 = k_hist_stream with one / two rings per CTA,
     "ws" = the warp-specialised k_hist_ws (stream kernels; order 2 takes k_hist_atomic)."""
     h = S.SinetHistogram(nets, lens, start, window, width, lut=lut, order=order)
@@ -45,6 +45,8 @@ def gpu_run(S, nets, lens, cols, start, window, width=1, lut=LUT_SRC_PRIORITY, o
         h.set_knob("stream_kernel", 1)
     h.set_tuning(groups, agg)
     h.set_table_mode(tab)
+    if scratch:   # unordered batches: partition then bin, sub-batches of `scratch` records
+        h.set_scratch(scratch)
     d = dev_cols(cols)
     n = d[0].numel()
     tg = torch.full((max(n, 4),), 0xEE, dtype=torch.uint8, device="cuda") if tags else None
@@ -221,6 +223,64 @@ def test_gaps_and_window_jumps(S, oracle_lib, strategy, groups):
     g = gpu_run(S, nets, lens, cols, start, window, order=strategy, groups=groups)
     o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, 1)
     assert_parity(g, o)
+
+
+# ----------------------------------------------------------------------------- partition then bin
+@pytest.mark.parametrize("width", [1, 3, 1000])
+@pytest.mark.parametrize("lut", [LUT_SRC_PRIORITY, LUT_ALG1])
+def test_partitioned_adversarial_parity(S, oracle_lib, lut, width):
+    """Unordered input through partition-then-bin (forced SHUFFLED + scratch): ragged sizes,
+    edge addresses, u64 bytes near 2^63 (the high-word accumulator), tags; scratch of 2^16
+    records makes the 200 k batch run as 4 sub-batches that add onto each other's tiles."""
+    nets, lens = prefix_table(WORKLOADS["c1"])
+    start, window = 1_613_660_400_000, 3_000_000
+    for n in (1, 5, 2047, 2049, 200_001):
+        cols = _adversarial(n, nets, lens, start, window, seed=3 * n + width)
+        g = gpu_run(S, nets, lens, cols, start, window, width, lut, order=2, tags=True, scratch=1 << 16)
+        assert g["h"].last_kernel.startswith("k_part")
+        o = oracle_lib.classify_histogram(*cols, nets, lens, start, window, width, lut=lut)
+        assert_parity(g, o)
+        np.testing.assert_array_equal(g["tags"], oracle_lib.tags(cols[0], cols[1], cols[2], nets, lens,
+                                                                 start, window))
+
+
+@pytest.mark.parametrize("name", ["c1", "c4", "c5"])
+def test_partitioned_workloads_parity(S, oracle_lib, name):
+    """Shuffled C1 (1 h), C4-shaped bursts with the 1 % hot millisecond (one fine bucket holds
+    ~1 % of all records: split into parts that add onto one tile) and the 4096-entry list."""
+    wl = WORKLOADS[name].with_(n=3_000_000 if name != "c1" else 1_000_000, order="shuffled")
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    for strategy in (0, 2):   # AUTO (the probe finds the order) and forced SHUFFLED
+        g = gpu_run(S, nets, lens, cols, wl.window_start_ms, wl.window_ms, order=strategy, scratch=1 << 22)
+        assert g["h"].last_kernel.startswith("k_part"), g["h"].last_kernel
+        assert_parity(g, o)
+    ts, src, dst, nb = cols
+    one = (np.full_like(ts, wl.window_start_ms + 1_800_000), src, dst, nb)   # every record in one ms
+    g = gpu_run(S, nets, lens, one, wl.window_start_ms, wl.window_ms, order=2, scratch=1 << 20)
+    assert_parity(g, oracle_lib.classify_histogram(*one, nets, lens, wl.window_start_ms, wl.window_ms, 1))
+
+
+def test_partitioned_watchlist_and_fallback(S, oracle_lib):
+    """NEXT-2 filter on the partitioned path; a window of more than 2^27 bins refuses scratch
+    and keeps the L2-atomic kernel."""
+    wl = WORKLOADS["c1"].with_(n=400_000, order="shuffled")
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    watch = np.unique(np.concatenate([cols[1][::97], cols[2][::89]]))
+    o = oracle_lib.classify_histogram_watched(*cols, nets, lens, watch, wl.window_start_ms, wl.window_ms, 1)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, order=2)
+    h.set_scratch(1 << 17)
+    h.set_watchlist(watch)
+    h.classify(*dev_cols(cols))
+    assert h.last_kernel.startswith("k_part")
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 0) for k in (0, 1)]), o.count)
+    np.testing.assert_array_equal(np.stack([h.read_bins(k, 1) for k in (0, 1)]), o.bytes)
+    np.testing.assert_array_equal(h.read_totals(), o.totals)
+    big = S.SinetHistogram(nets, lens, wl.window_start_ms, (1 << 27) + 8192, order=2)
+    with pytest.raises(S.SinetError):
+        big.set_scratch(1 << 16)
 
 
 def test_chunked_accumulation_and_reset(S, oracle_lib):
