@@ -227,8 +227,9 @@ int sinet_nccl_unique_id(void* out128);
  * rendezvous on a host barrier; device order is kept with CUDA events).  Data moves by
  * peer copies over UVA, and the dense reduce-scatter is one kernel per owner reading its
  * slice from every rank's bins directly (NVLink P2P loads between GPUs; peer access is
- * enabled on first use).  Results are identical to the NCCL path.  The hub must outlive
- * every ctx attached to it; a ctx attaches once (sinet_close detaches it).
+ * enabled on first use).  Results are identical to the NCCL path.  The hub is reference
+ * counted: sinet_hub_destroy drops the creator's reference and the memory is freed when the
+ * last attached ctx closes (in any order); a ctx attaches once (sinet_close detaches it).
  * Errors: E_INVAL (world < 1 or > 64, NULL out / hub, hub world != cfg.world, rank already
  * attached), E_STATE (ctx already has a communicator). */
 int sinet_hub_create(sinet_hub** out, int32_t world);
@@ -413,6 +414,10 @@ int sinet_table_mode(const sinet_ctx* ctx);
 /* Compile-time constants of this build. */
 uint32_t sinet_tile_bins(void);
 uint32_t sinet_parse_chunk_bytes(void);   /* text bytes one CTA of sinet_parse_text owns per ticket */
+/* Process-wide performance/test knob of sinet_parse_text (results identical for every value):
+ * "unpacked_look_back" 1 forces the two-word look-back used for >= 2 GiB of text.  E_INVAL
+ * for an unknown name or value. */
+int sinet_parse_set_knob(const char* name, int64_t value);
 int sinet_abi_version(void);
 
 #ifdef __cplusplus

@@ -121,6 +121,7 @@ _SIGS = {
     "sinet_parse_text": ([_vp, _u64, ctypes.c_int32, ctypes.POINTER(Columns), _vp, _u64, _vp, ctypes.c_size_t, _vp,
                           ctypes.POINTER(ParseResult)], _i),
     "sinet_parse_last_error": ([], ctypes.c_char_p),
+    "sinet_parse_set_knob": ([ctypes.c_char_p, ctypes.c_int64], _i),
     "sinet_table_member_host_labelled": ([_vp, _vp, _vp, _u32, _vp, _u64, _vp], _i),
 }
 for _name, (_args, _res) in _SIGS.items():

@@ -370,6 +370,10 @@ void plan_exchange(int world, int rank, uint64_t B, uint64_t B_pad, const uint32
     for (int r = 0; r < world; ++r) (*recv)[r] = inter(r, rank);
 }
 
+namespace {
+std::atomic<bool> g_parse_unpacked{false};   // sinet_parse_set_knob("unpacked_look_back")
+}  // namespace
+
 extern "C" {
 
 int sinet_exchange_plan(int32_t world, int32_t rank, uint64_t nbins, uint64_t nbins_pad, const uint32_t* touched,
@@ -1076,7 +1080,16 @@ extern "C" size_t sinet_parse_workspace_bytes(uint64_t text_bytes) {
 
 extern "C" const char* sinet_parse_last_error(void) { return g_parse_err.c_str(); }
 
-extern "C" int sinet_parse_text(const uint8_t* d_text, uint64_t text_bytes, int32_t tz_offset_min,
+extern "C" int sinet_parse_set_knob(const char* name, int64_t value) {
+    if (!name) return SINET_E_INVAL;
+    if (std::string(name) == "unpacked_look_back" && (value == 0 || value == 1)) {
+        g_parse_unpacked.store(value != 0, std::memory_order_relaxed);
+        return SINET_OK;
+    }
+    return SINET_E_INVAL;
+}
+
+int sinet_parse_text(const uint8_t* d_text, uint64_t text_bytes, int32_t tz_offset_min,
                                 const sinet_columns* out, uint8_t* d_status, uint64_t status_capacity,
                                 void* d_ws, size_t ws_bytes, void* stream, sinet_parse_result* result) {
     g_parse_err.clear();
@@ -1115,7 +1128,7 @@ extern "C" int sinet_parse_text(const uint8_t* d_text, uint64_t text_bytes, int3
     p.st_valid = p.st_lines + nch;
     p.n_chunks = nch;
     p.packed = text_bytes < (1ull << 31) ? 1u : 0u;
-    if (const char* u = std::getenv("SINET_PARSE_UNPACKED")) if (std::atoi(u)) p.packed = 0u;   // test hook
+    if (g_parse_unpacked.load(std::memory_order_relaxed)) p.packed = 0u;   // knob "unpacked_look_back"
     if (e == cudaSuccess && nch) e = launch_parse_text(p, parse_sm_count(), st);
     unsigned long long h[10] = {0};
     unsigned long long last[2] = {0, 0};

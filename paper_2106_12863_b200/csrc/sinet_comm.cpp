@@ -150,6 +150,7 @@ struct sinet_hub {
     };
     explicit sinet_hub(int w) : world(w), slot((size_t)w) {}
     int world;
+    int refs = 1;          // the creator's reference + one per attached rank (freed at zero)
     std::mutex mu;
     std::condition_variable cv;
     uint64_t generation = 0;
@@ -185,8 +186,13 @@ public:
             if (s.done[k]) cudaEventDestroy(s.done[k]);
             s.ready[k] = s.done[k] = nullptr;
         }
-        std::lock_guard<std::mutex> lk(hub_->mu);
-        s.attached = false;
+        bool last;
+        {
+            std::lock_guard<std::mutex> lk(hub_->mu);
+            s.attached = false;
+            last = --hub_->refs == 0;
+        }
+        if (last) delete hub_;   // sinet_hub_destroy ran first: the last rank frees the hub
     }
     int init(std::string* err) {
         auto& s = hub_->slot[(size_t)rank_];
@@ -347,6 +353,7 @@ std::unique_ptr<Transport> make_hub_transport(sinet_hub* hub, int rank, int devi
         std::lock_guard<std::mutex> lk(hub->mu);
         if (hub->slot[(size_t)rank].attached) { *err = "hub: rank already attached"; return nullptr; }
         hub->slot[(size_t)rank].attached = true;
+        ++hub->refs;
     }
     std::unique_ptr<HubTransport> t(new HubTransport(hub, rank, device));
     if (t->init(err) != SINET_OK) return nullptr;
@@ -363,6 +370,14 @@ int sinet_hub_create(sinet_hub** out, int32_t world) {
     return *out ? SINET_OK : SINET_E_INVAL;
 }
 
-void sinet_hub_destroy(sinet_hub* hub) { delete hub; }
+void sinet_hub_destroy(sinet_hub* hub) {
+    if (!hub) return;
+    bool last;
+    {
+        std::lock_guard<std::mutex> lk(hub->mu);
+        last = --hub->refs == 0;
+    }
+    if (last) delete hub;   // else the last attached ctx frees it when it closes
+}
 
 }  // extern "C"

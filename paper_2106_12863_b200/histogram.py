@@ -256,10 +256,13 @@ class SinetHistogram:
         return lo.value, lo.value + n.value
 
     # ------------------------------------------------------------------ read-out
-    def read_bins(self, direction: int, metric: int, first: int = 0, n: int | None = None,
+    def read_bins(self, direction: int, metric: int, first: int | None = None, n: int | None = None,
                   device: bool = False):
-        """u64 plane slice as numpy uint64 (host) or a torch int64 tensor (device)."""
+        """u64 plane slice [first, first + n) (default: the whole owned range) as numpy uint64
+        (host) or a torch int64 tensor (device)."""
         lo, hi = self.owned_range()
+        if first is None:
+            first = lo
         if n is None:
             n = hi - first
         if device:

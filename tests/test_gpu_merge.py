@@ -64,7 +64,7 @@ def _run_world(S, wl, world, exchange, order_t, own_streams=True):
         except Exception as e:  # noqa: BLE001
             errs[r] = e
 
-    th = [threading.Thread(target=reduce, args=(r,)) for r in range(world)]
+    th = [threading.Thread(target=reduce, args=(r,), daemon=True) for r in range(world)]
     for t in th:
         t.start()
     for t in th:
@@ -149,7 +149,7 @@ def test_hub_merge_sparse_overlapping_and_empty_ranks(S, oracle_lib):
             hs[r].classify(*cols)
         torch.cuda.synchronize()
     errs = []
-    th = [threading.Thread(target=lambda h=h: (errs.append(None), h.reduce())) for h in hs]
+    th = [threading.Thread(target=lambda h=h: (errs.append(None), h.reduce()), daemon=True) for h in hs]
     for t in th:
         t.start()
     for t in th:
@@ -197,7 +197,7 @@ def test_hub_repeated_days_same_ctxs(S, oracle_lib):
         lo, hi = S.shard_range(wl.n, r, 3)
         with torch.cuda.stream(h.stream):
             h.classify(rec["ts"][lo:hi], rec["src"][lo:hi], rec["dst"][lo:hi], rec["bytes"][lo:hi])
-    th = [threading.Thread(target=h.reduce) for h in hs]
+    th = [threading.Thread(target=h.reduce, daemon=True) for h in hs]
     for t in th:
         t.start()
     for t in th:

@@ -101,13 +101,17 @@ def test_lines_across_chunk_boundaries_and_long_lines():
         check_against_oracle(blob[:len(blob) - cut] + b"\n")
 
 
-def test_unpacked_look_back(monkeypatch):
+def test_unpacked_look_back():
     """Texts of 2 GiB or more scan lines and valid records in two look-back words per chunk
-    (one packed word below that); the hook forces the two-word path on a small text."""
-    monkeypatch.setenv("SINET_PARSE_UNPACKED", "1")
-    blob, _ = gen_text(20_000, bad=50_000)
-    check_against_oracle(blob)
-    check_against_oracle(b"\n" * (3 * CHUNK + 5))
+    (one packed word below that); the knob forces the two-word path on a small text."""
+    from paper_2106_12863_b200 import _native as N
+    assert N.lib.sinet_parse_set_knob(b"unpacked_look_back", 1) == 0
+    try:
+        blob, _ = gen_text(20_000, bad=50_000)
+        check_against_oracle(blob)
+        check_against_oracle(b"\n" * (3 * CHUNK + 5))
+    finally:
+        N.lib.sinet_parse_set_knob(b"unpacked_look_back", 0)
 
 
 def test_fuzzed_lines():

@@ -1,6 +1,7 @@
 #!/bin/bash
 # One parameterised GPU job for gpurun:  gpurun -- bash tools/gpu_run.sh TAG STEP [STEP ...]
-# Steps: smoke pytest pytest_merge bench ref c1 c3 c4 c5 shuf launches ncu_c2 ncu_c4 ncu_c5 san digests
+# Steps: smoke pytest pytest_merge pytest_new bench benchws ref c1..c5 shuf launches ncu_c2 ncu_c4 ncu_c5
+#        ncu_ws ncu_ws_c4 san wscheck
 # Every output lands in gpurun_out/TAG_<step>.txt (merged back by gpurun).
 set -x
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
@@ -14,7 +15,7 @@ for s in "$@"; do
   case $s in
     smoke) timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > ${O}_smoke.txt 2>&1 ;;
     pytest) timeout 2400 python -m pytest tests -m gpu -q -x --timeout 1200 > ${O}_pytest_gpu.txt 2>&1 ;;
-    pytest_merge) timeout 1200 python -m pytest tests/test_gpu_merge.py -m gpu -q -x --timeout 900 > ${O}_pytest_merge.txt 2>&1 ;;
+    pytest_merge) timeout 900 python -m pytest tests/test_gpu_merge.py -m gpu -q --timeout 300 > ${O}_pytest_merge.txt 2>&1 ;;
     bench) timeout 1200 python bench.py > ${O}_bench.txt 2>&1 ;;
     ref) timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > ${O}_ref.txt 2>&1 ;;
     c1|c2|c3|c4|c5) $B --config $s > ${O}_$s.txt 2>&1 ;;
@@ -25,7 +26,11 @@ for s in "$@"; do
     ncu_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile > ${O}_ncu_c4_run.txt 2>&1 ;;
     ncu_c5) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c5 python bench.py --config c5 --steps 2 --warmup 1 --profile > ${O}_ncu_c5_run.txt 2>&1 ;;
     san) for t in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $t python tools/sanitize_case.py > ${O}_san_$t.txt 2>&1; done ;;
-    digests) timeout 2400 python tools/oracle_digests.py --check-gpu > ${O}_digests.txt 2>&1 ;;
+    wscheck) timeout 900 python tools/ws_check.py > ${O}_wscheck.txt 2>&1 ;;
+    pytest_new) timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 300 -k "ws or partitioned or bursty or gaps or dense or c1_full or table_enc or inline" > ${O}_pytest_new.txt 2>&1 ;;
+    ncu_ws) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_ws -s 2 -c 1 -o ${O}_prof_ws python bench.py --steps 2 --warmup 1 --profile --knob stream_kernel=2 > ${O}_ncu_ws_run.txt 2>&1 ;;
+    ncu_ws_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_ws -s 2 -c 1 -o ${O}_prof_ws_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile --knob stream_kernel=2 > ${O}_ncu_ws_c4_run.txt 2>&1 ;;
+    benchws) timeout 1800 python bench.py --knob stream_kernel=2 > ${O}_benchws.txt 2>&1 ;;
     *) echo "unknown step $s" ;;
   esac
 done
