@@ -87,6 +87,10 @@ __device__ __forceinline__ uint32_t ring_add(uint32_t a, uint32_t cnt, uint64_t 
 
 }  // namespace
 
+// diagnostics (sinet_debug_counters): [0] late records, [1] early records, [2] high-word spills,
+// [3] retire batches, [4] tiles retired, [5] manager idle polls, [6] chunks, [7] hot chunks
+__device__ unsigned long long g_ws_dbg[8];
+
 template <int WS, int kTab, bool kW1, bool kWatch>
 __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
     constexpr uint32_t NT = WS / kTileBins;       // resident tiles
@@ -253,6 +257,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                     bool any = false;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) any |= dir4[j] < 2u || hi4[j] != 0u;
+                    if (p.debug) {
+                        uint32_t late = 0, early = 0, hiw = 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (dir4[j] < 2u) { if (bin4[j] / kTileBins < lo) ++late; else ++early; }
+                            if (hi4[j]) ++hiw;
+                        }
+                        late = __reduce_add_sync(kFull, late); early = __reduce_add_sync(kFull, early);
+                        hiw = __reduce_add_sync(kFull, hiw);
+                        if (lane == 0) { atomicAdd(&g_ws_dbg[0], late); atomicAdd(&g_ws_dbg[1], early); atomicAdd(&g_ws_dbg[2], hiw); }
+                    }
                     if (__any_sync(kFull, any)) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -297,6 +312,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                 bmax = __reduce_max_sync(kFull, bmax);
                 head = max(head, bmax / kTileBins);
                 __syncwarp();
+                if (p.debug && lane == 0) { atomicAdd(&g_ws_dbg[6], 1ull); if (key0 == key3) atomicAdd(&g_ws_dbg[7], 1ull); }
                 if (lane == 0) {
                     *reinterpret_cast<volatile uint32_t*>(&s_head[warp]) = head;
                     sts_release(&s_used[warp], lo);
@@ -314,8 +330,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
             if (lane == 0) sts_release(&s_done[warp], 1u);   // s_head keeps this warp's final newest tile
         } else {
             // ================================================================ manager
-            uint32_t lo = s_lo, raised = lo, hull_hi = lo;
-            bool hs = false;              // a raise of lo awaits the workers' handshake
+            // retired: the oldest resident tile; lo_pub: the published lower edge (raised
+            // eagerly); a tile below every worker's acknowledged lo (s_used) is retired.  The
+            // batch is everything that became safe, so a manager that falls behind catches up
+            // with larger batches (one claim round trip + one completion wait per batch).
+            uint32_t retired = s_lo, lo_pub = retired, hull_hi = retired;
             unsigned pub_m = 0u;          // won tiles of the last batch, published after their bulk stores
             uint32_t pub_base = 0u;
             auto publish = [&]() {
@@ -337,17 +356,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                 if (lane == 0 && nstage >= 2u) bulk_wait_read<1>();   // the buffer's previous bulk read is done
                 __syncwarp();
                 ulonglong2* st = reinterpret_cast<ulonglong2*>(s_stage) + b * (kTileBins * 2u);
+                const uint32_t s0 = (t * kTileBins) & (WS - 1);
 #pragma unroll 4
                 for (uint32_t i = lane; i < kTileBins; i += 32u) {
-                    const uint32_t slot = (t * kTileBins + i) & (WS - 1);
-                    uint2* sc = reinterpret_cast<uint2*>(s_win + slot * 2u);
-                    uint2* sl = reinterpret_cast<uint2*>(s_win + kLoOff + slot * 2u);
-                    const uint2 c = *sc, l = *sl;
-                    *sc = make_uint2(0u, 0u);
-                    *sl = make_uint2(0u, 0u);
+                    const uint2 c = *reinterpret_cast<const uint2*>(s_win + (s0 + i) * 2u);
+                    const uint2 l = *reinterpret_cast<const uint2*>(s_win + kLoOff + (s0 + i) * 2u);
                     st[i * 2u] = make_ulonglong2(c.x, l.x);
                     st[i * 2u + 1u] = make_ulonglong2(c.y, l.y);
                 }
+                __syncwarp();
+                // zero the tile's ring slots: 2 KB of counts + 2 KB of low words, 128-bit stores
+                uint4* zc = reinterpret_cast<uint4*>(s_win + s0 * 2u);
+                uint4* zl = reinterpret_cast<uint4*>(s_win + kLoOff + s0 * 2u);
+#pragma unroll
+                for (uint32_t i = lane; i < kTileBins / 2u; i += 32u) { zc[i] = make_uint4(0u, 0u, 0u, 0u); zl[i] = make_uint4(0u, 0u, 0u, 0u); }
                 fence_async_smem();
                 __syncwarp();
                 return stage_base + b * kStageBytes;
@@ -361,11 +383,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                 }
                 ++nstage;
             };
-            // retire tiles [t0, t1) (handshake complete: no worker touches them any more)
+            // retire tiles [t0, t1), t1 - t0 <= NT <= 32 (no worker touches them any more)
             auto retire = [&](uint32_t t0, uint32_t t1) {
                 const uint32_t n = t1 - t0;
                 uint32_t o = 0u;
-                if (lane < n && t0 + lane <= hull_hi) {
+                if (lane < n && t0 + lane <= hull_hi) {   // tiles beyond the hull hold no data
                     uint32_t* f = p.tile_flags + t0 + lane;
                     o = claim_outcome(f, p.epoch, prev_word, atomicCAS(f, prev_word, claimed_word));
                 }
@@ -375,11 +397,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                     const uint32_t kk = (uint32_t)(__ffs(m) - 1);
                     issue(t0 + kk, (won_m >> kk) & 1u, convert(t0 + kk));
                 }
-                // tiles beyond the hull hold no data (their ring slots are zero)
                 pub_m = won_m;
                 pub_base = t0;
                 if (busy_m) {
-                    // claimed elsewhere, not yet initialised: publish ours first, then wait
+                    // claimed elsewhere, not yet initialised: publish ours first (we then hold no
+                    // claim), wait for the claimer, add
                     publish();
                     for (unsigned m = busy_m; m; m &= m - 1u) {
                         const uint32_t kk = (uint32_t)(__ffs(m) - 1);
@@ -393,37 +415,37 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_hist_ws(KernelParams p) {
                         __syncwarp();
                         issue(t0 + kk, false, convert(t0 + kk));
                     }
-                    if (lane == 0) bulk_wait_read<0>();
-                    __syncwarp();
                 }
             };
             for (;;) {
                 publish();
                 const bool dn = (lane < kWorkers) ? lds_acquire(&s_done[lane]) != 0u : true;
-                const uint32_t used = (lane < kWorkers) ? lds_acquire(&s_used[lane]) : 0u;
+                const uint32_t used = (lane < kWorkers) ? lds_acquire(&s_used[lane]) : kDone;
                 const uint32_t hd = (lane < kWorkers) ? lds_volatile(&s_head[lane]) : 0u;
                 const bool all_done = __all_sync(kFull, dn);
                 const uint32_t hmin = __reduce_min_sync(kFull, dn ? kDone : hd);   // finished workers do not pin the window
                 hull_hi = max(hull_hi, __reduce_max_sync(kFull, hd));
-                if (hs && __all_sync(kFull, dn || used >= raised)) {
+                // raise the lower edge as far as the slowest worker's history allows
+                uint32_t target = retired;
+                if (all_done) target = min(retired + NT, hull_hi + 1u);
+                else if (hmin >= retired + kHist) target = min(retired + NT, hmin - kHist);
+                if (target > lo_pub) {
+                    lo_pub = target;
+                    if (lane == 0) sts_release(&s_lo, lo_pub);
+                }
+                // retire what every worker has acknowledged
+                const uint32_t safe = all_done ? lo_pub : min(lo_pub, __reduce_min_sync(kFull, dn ? kDone : used));
+                if (safe >= retired + (all_done ? 1u : kBatch)) {
                     __syncwarp();   // every lane's ring reads after the workers' releases (acquired above)
-                    retire(lo, raised);
-                    lo = raised;
-                    if (lane == 0) sts_release(&s_top, lo + NT);
-                    hs = false;
+                    if (p.debug && lane == 0) { atomicAdd(&g_ws_dbg[3], 1ull); atomicAdd(&g_ws_dbg[4], (unsigned long long)(safe - retired)); }
+                    retire(retired, safe);
+                    retired = safe;
+                    __syncwarp();
+                    if (lane == 0) sts_release(&s_top, retired + NT);
+                    continue;
                 }
-                if (!hs) {
-                    uint32_t target = lo;
-                    if (all_done) target = min(lo + NT, hull_hi + 1u);
-                    else if (hmin >= lo + kHist + kBatch) target = min(lo + NT, hmin - kHist);
-                    if (target > lo) {
-                        if (lane == 0) sts_release(&s_lo, target);
-                        raised = target;
-                        hs = true;
-                        continue;
-                    }
-                    if (all_done) break;
-                }
+                if (all_done && lo_pub == retired) break;
+                if (p.debug && lane == 0) atomicAdd(&g_ws_dbg[5], 1ull);
                 __nanosleep(32);
             }
             publish();
@@ -462,6 +484,15 @@ cudaError_t setup_hist_ws() {
 }
 
 // the ring this table leaves room for: 8192 bins (32 tiles), else 4096
+extern "C" int sinet_debug_counters(unsigned long long* out8, int reset) {
+    if (out8 && cudaMemcpyFromSymbol(out8, g_ws_dbg, sizeof(g_ws_dbg)) != cudaSuccess) return -4;
+    if (reset) {
+        static const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (cudaMemcpyToSymbol(g_ws_dbg, z, sizeof(z)) != cudaSuccess) return -4;
+    }
+    return 0;
+}
+
 int hist_ws_ring_bins(int tab, uint32_t nbnd, uint32_t n_mixed) {
     return (ring_smem(8192) + stream_table_bytes(tab, nbnd, n_mixed) <= kMaxDynSmem) ? 8192 : 4096;
 }

@@ -256,6 +256,22 @@ class SinetHistogram:
         return lo.value, lo.value + n.value
 
     # ------------------------------------------------------------------ read-out
+    def _take_over(self):
+        """Buffers the caller allocated on its current stream: the ctx stream waits for it first."""
+        cur = torch.cuda.current_stream(self.device)
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+
+    def _hand_over(self, *tensors):
+        """Device results written on the ctx stream: the caller's current stream waits for it,
+        and the caching allocator keeps the buffers until the ctx stream is done with them."""
+        cur = torch.cuda.current_stream(self.device)
+        if cur != self.stream:
+            cur.wait_stream(self.stream)
+            for t in tensors:
+                if t is not None and t.is_cuda:
+                    t.record_stream(self.stream)
+
     def read_bins(self, direction: int, metric: int, first: int | None = None, n: int | None = None,
                   device: bool = False):
         """u64 plane slice [first, first + n) (default: the whole owned range) as numpy uint64
@@ -267,12 +283,15 @@ class SinetHistogram:
             n = hi - first
         if device:
             out = torch.empty(n, dtype=torch.int64, device=self.device)
+            self._take_over()
             ptr = _ptr(out)
         else:
             out = np.empty(n, dtype=np.uint64)
             ptr = out.ctypes.data_as(ctypes.c_void_p)
         check(lib.sinet_read_bins(self.ctx, direction, metric, first, n, ptr, 1 if device else 0),
               self.ctx, "read_bins")
+        if device:
+            self._hand_over(out)
         return out
 
     def read_bins_raw(self, out: torch.Tensor | None = None, first: int | None = None, n: int | None = None):
@@ -285,7 +304,11 @@ class SinetHistogram:
             out = torch.empty((n, 2, 2), dtype=torch.int64)
         assert out.dtype == torch.int64 and out.is_contiguous() and out.numel() >= 4 * n
         dev = out.device.type == "cuda"
+        if dev:
+            self._take_over()
         check(lib.sinet_read_bins_raw(self.ctx, first, n, _ptr(out), 1 if dev else 0), self.ctx, "read_bins_raw")
+        if dev:
+            self._hand_over(out)
         return out
 
     def rebin_frames(self, factor: int):
@@ -300,7 +323,9 @@ class SinetHistogram:
         owned bins of frame rebin_frames()[0] + k (frames aligned to the window start)."""
         _, n_out = self.rebin_frames(factor)
         out = torch.empty((max(n_out, 1), 2, 2), dtype=torch.int64, device=self.device)
+        self._take_over()
         check(lib.sinet_rebin(self.ctx, int(factor), _ptr(out), n_out), self.ctx, "rebin")
+        self._hand_over(out)
         return out[:n_out]
 
     def set_knob(self, name: str, value: int):
@@ -315,8 +340,10 @@ class SinetHistogram:
                   self.ctx, "export_sparse")
             capacity = n.value
         bufs = [torch.empty(max(capacity, 1), dtype=torch.int64, device=self.device) for _ in range(3)]
+        self._take_over()
         check(lib.sinet_export_sparse(self.ctx, direction, _ptr(bufs[0]), _ptr(bufs[1]), _ptr(bufs[2]), capacity,
                                       ctypes.byref(n)), self.ctx, "export_sparse")
+        self._hand_over(*bufs)
         k = min(n.value, capacity)
         return tuple(b[:k] for b in bufs), n.value
 

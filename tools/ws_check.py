@@ -54,6 +54,25 @@ for name, n in (("c1", 300_000), ("c2", 3_000_000), ("c4", 3_000_000), ("c5", 2_
         print(f"parity {name} n={n} kernel={kern} ({h.last_kernel}): {'OK' if ok else 'MISMATCH'} {time.time()-t0:.1f}s",
               flush=True)
         h.close()
+import ctypes
+from paper_2106_12863_b200 import _native as N
+N.lib.sinet_debug_counters.argtypes = [ctypes.c_void_p, ctypes.c_int]
+dbg = (ctypes.c_ulonglong * 8)()
+for name in ("c2", "c4"):
+    wl = WORKLOADS[name].with_(n=100_000_000)
+    rec = records_into(wl, 0, wl.n, "cuda")
+    nets, lens = prefix_table(wl)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, order=S.ORDER_STREAM)
+    h.set_knob("stream_kernel", 2)
+    h.set_knob("debug_counters", 1)
+    N.lib.sinet_debug_counters(None, 1)
+    h.classify(rec["ts"], rec["src"], rec["dst"], rec["bytes"])
+    torch.cuda.synchronize()
+    N.lib.sinet_debug_counters(dbg, 1)
+    print("debug", name, "late, early, hi, batches, tiles, idle polls, chunks, hot chunks =", list(dbg), flush=True)
+    h.close()
+    del rec
+    torch.cuda.empty_cache()
 for name in ("c2", "c4", "c5"):
     wl = WORKLOADS[name]
     if name == "c4":
