@@ -57,8 +57,8 @@ for name, n in (("c1", 300_000), ("c2", 3_000_000), ("c4", 3_000_000), ("c5", 2_
 import ctypes
 from paper_2106_12863_b200 import _native as N
 N.lib.sinet_debug_counters.argtypes = [ctypes.c_void_p, ctypes.c_int]
-dbg = (ctypes.c_ulonglong * 8)()
-for name in ("c2", "c4"):
+dbg = (ctypes.c_ulonglong * 12)()
+for name in ("c2",):
     wl = WORKLOADS[name].with_(n=100_000_000)
     rec = records_into(wl, 0, wl.n, "cuda")
     nets, lens = prefix_table(wl)
@@ -69,7 +69,7 @@ for name in ("c2", "c4"):
     h.classify(rec["ts"], rec["src"], rec["dst"], rec["bytes"])
     torch.cuda.synchronize()
     N.lib.sinet_debug_counters(dbg, 1)
-    print("debug", name, "late, early, hi, batches, tiles, idle polls, chunks, hot chunks =", list(dbg), flush=True)
+    print("debug", name, "late, early, hi, batches, tiles, idle polls, chunks, hot chunks, wait heads, wait handshake, sum(tile-top) early, max head spread =", list(dbg), flush=True)
     h.close()
     del rec
     torch.cuda.empty_cache()
