@@ -88,6 +88,17 @@ __global__ void __launch_bounds__(256) k_hist_atomic(KernelParams p) {
     flush_totals(tot, p.totals, s_tot);
 }
 
+// AUTO order probe: run k of kProbeRun consecutive ts starting at (n - kProbeRun) * k / (kProbeRuns - 1)
+__global__ void k_probe_gather(const uint64_t* __restrict__ ts, uint64_t n, uint64_t* __restrict__ out) {
+    const uint64_t at = (n - kProbeRun) * (uint64_t)blockIdx.x / (kProbeRuns - 1);
+    out[blockIdx.x * kProbeRun + threadIdx.x] = ts[at + threadIdx.x];
+}
+
+cudaError_t launch_probe_gather(const uint64_t* ts, uint64_t n, uint64_t* out, cudaStream_t st) {
+    k_probe_gather<<<kProbeRuns, kProbeRun, 0, st>>>(ts, n, out);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32_t n_tiles,
                                uint32_t init_word, int grid, cudaStream_t st) {

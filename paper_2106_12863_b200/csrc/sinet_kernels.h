@@ -13,6 +13,10 @@ cudaError_t launch_materialize(unsigned long long* bins, uint32_t* flags, uint32
 cudaError_t launch_materialize_range(unsigned long long* bins, uint32_t* flags, uint32_t t_lo, uint32_t t_hi,
                                      uint32_t init_word, int grid, cudaStream_t st);
 
+// AUTO order probe: kProbeRuns evenly spaced runs of kProbeRun consecutive capture times
+constexpr uint32_t kProbeRuns = 64, kProbeRun = 32;
+cudaError_t launch_probe_gather(const uint64_t* ts, uint64_t n, uint64_t* out, cudaStream_t st);
+
 cudaError_t setup_hist_atomic();
 int hist_atomic_blocks_per_sm(const KernelParams& p);
 cudaError_t launch_hist_atomic(const KernelParams& p, int grid, cudaStream_t st);

@@ -44,7 +44,7 @@ template <int THREADS, int NG, int WS, int RPT, bool kAgg, bool kW1, int kTab, b
 __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // RPT records per thread per chunk; with RPT == 2 the side totals live in shared
     // memory per warp (registers for 1024 threads)
-    constexpr bool kSmemTot = (RPT == 2);
+    constexpr bool kSmemTot = (RPT == 2 || THREADS > 512);   // totals per warp in shared memory (registers)
     using Rec = typename RecN<RPT>::T;
     constexpr int GT = THREADS / NG;          // threads per group
     constexpr int NW = THREADS / 32;
@@ -338,7 +338,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         uint32_t hi4[RPT];   // high words owed to HBM (added after the barrier)
 #pragma unroll
         for (int j = 0; j < RPT; ++j) hi4[j] = 0u;
-        if (!kAgg && have_window) {
+        // (knob hot_agg) a hot warp-chunk -- its first and last record in the same (bin, dir), a hot
+        // millisecond -- aggregates equal keys before the shared-memory atomics, which would
+        // otherwise serialise 32-way on one address
+        const bool hot = !kAgg && p.hot_agg && p.nbins < 0x40000000u &&
+                         __shfl_sync(kFull, dir4[0] < 2u ? (bin4[0] << 1) | dir4[0] : 0xFFFFFFFFu, 0) ==
+                             __shfl_sync(kFull, dir4[RPT - 1] < 2u ? (bin4[RPT - 1] << 1) | dir4[RPT - 1] : 0xFFFFFFFEu, 31);
+        if (!kAgg && have_window && !hot) {
             bool take[RPT];
 #pragma unroll
             for (int j = 0; j < RPT; ++j) take[j] = dir4[j] < 2u && bin4[j] / kTileBins - act_t < lo_t + NT - act_t;
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         // ---- a6 (accumulate): reduce the chunk into the ring
         // the whole chunk inside the ring (the common case): no per-record residency/spill checks
         const bool all_in = any && bmin_t >= lo_t && bmax_t - lo_t < NT;
-        if (!kAgg && all_in) {
+        if (!kAgg && all_in && !hot) {
             bool rest[RPT];
             bool any_rest = false;
 #pragma unroll
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             // cheap neighbour test finds a duplicate in the warp (records of one slot are
             // RPT apart in stream order, so hot keys show up in adjacent lanes)
             bool try_agg = false;
-            if (kAgg) {
+            if (kAgg || hot) {
                 const uint32_t k32 = b ? ((bin4[j] << 1) | dir4[j]) : 0xFFFFFFFFu - lane;
                 const uint32_t kp = __shfl_up_sync(kFull, k32, 1);
                 try_agg = __any_sync(kFull, b && lane > 0u && kp == k32);
@@ -497,9 +503,20 @@ constexpr int kRingBins2 = 4096;
     k_hist_stream<512, G, (G == 1 ? kRingBins1 : kRingBins2), 4, A, W, S, WL>
 constexpr size_t kRingSmem = (size_t)kRingBins1 * 4u * 4u;   // 128 KB: 4 u32 per bin
 
+// experimental: 640 threads (2 groups of 10 warps), totals in shared memory (<= 102 registers)
+#define SINET_STREAM_KERNEL640(W, S) k_hist_stream<640, 2, kRingBins2, 4, false, W, S, false>
+
 cudaError_t setup_hist_stream() {
     const int mx = (int)(kRingSmem + kStreamTableSmem);
     cudaError_t e;
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(true, kTabByte), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(false, kTabByte), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(true, kTabPackedNoL2), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(false, kTabPackedNoL2), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
 #define SET(G, A, W, S, WL)                                                                                 \
     e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W, S, WL), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
@@ -536,6 +553,16 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
     cudaError_t e = cudaMemsetAsync(p.range_counter, 0, 8, st);
     if (e != cudaSuccess) return e;
+    if (p.block_threads == 640u && g == 2 && !agg && p.wn == 0u && (tab == kTabByte || tab == kTabPackedNoL2)) {
+        if (tab == kTabByte) {
+            if (w1) SINET_STREAM_KERNEL640(true, kTabByte)<<<grid, 640, sm, st>>>(q);
+            else SINET_STREAM_KERNEL640(false, kTabByte)<<<grid, 640, sm, st>>>(q);
+        } else {
+            if (w1) SINET_STREAM_KERNEL640(true, kTabPackedNoL2)<<<grid, 640, sm, st>>>(q);
+            else SINET_STREAM_KERNEL640(false, kTabPackedNoL2)<<<grid, 640, sm, st>>>(q);
+        }
+        return cudaGetLastError();
+    }
 #define LAUNCH(G, S, WL)                                                                                \
     if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S, WL)<<<grid, 512, sm, st>>>(q);                  \
     else if (agg) SINET_STREAM_KERNEL(G, true, false, S, WL)<<<grid, 512, sm, st>>>(q);                  \

@@ -293,7 +293,7 @@ def _feistel_perm(j: torch.Tensor, n: int, seed: int) -> torch.Tensor:
     x = j.clone()
     todo = torch.ones_like(x, dtype=torch.bool)
     out = x.clone()
-    for _ in range(64):
+    for _ in range(512):   # (1 - n / 2^bits)^512 < 1e-70: every element has left the cycle walk
         l, r = x >> h, x & hm
         for rnd in range(4):
             f = rand64(seed, S_PERM + 1000 * rnd, r) & hm
