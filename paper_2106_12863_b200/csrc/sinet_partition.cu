@@ -261,11 +261,19 @@ __global__ void __launch_bounds__(kPT, 1) k_part_scatter(KernelParams p, PartArg
     tot.zero();
     uint32_t gmin = 0xFFFFFFFFu, gmax = 0u;
     const bool tags_on = p.tags != nullptr;
-    for (uint64_t cb = (uint64_t)blockIdx.x * kPChunk; cb < p.nv; cb += (uint64_t)gridDim.x * kPChunk) {
-        const uint64_t my_v = cb + threadIdx.x * 4u;
-        Rec4 r;
-        if (my_v < p.nv) load4(p, my_v, r);
+    // the next chunk's records are loaded into registers while this one is sorted and written
+    const uint64_t stride = (uint64_t)gridDim.x * kPChunk;
+    Rec4 nxt;
+    auto load_chunk = [&](uint64_t cb, Rec4& r) {
+        const uint64_t v = cb + threadIdx.x * 4u;
+        if (v < p.nv) load4(p, v, r);
         else { for (int j = 0; j < 4; ++j) { r.ts[j] = 0; r.src[j] = r.dst[j] = 0; r.by[j] = 0; } }
+    };
+    if ((uint64_t)blockIdx.x * kPChunk < p.nv) load_chunk((uint64_t)blockIdx.x * kPChunk, nxt);
+    for (uint64_t cb = (uint64_t)blockIdx.x * kPChunk; cb < p.nv; cb += stride) {
+        const uint64_t my_v = cb + threadIdx.x * 4u;
+        const Rec4 r = nxt;
+        if (cb + stride < p.nv) load_chunk(cb + stride, nxt);
         uint32_t addr[8], in8[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) { addr[2 * j] = r.src[j]; addr[2 * j + 1] = r.dst[j]; }
@@ -369,6 +377,18 @@ __global__ void __launch_bounds__(kPT, 1) k_part_bin(KernelParams p, PartArgs a)
         const uint32_t f = lo - 1;
         const uint32_t r0 = a.fine_base[f] + (u - a.unit_base[f]) * kPartRecords;
         const uint32_t r1 = min(r0 + kPartRecords, a.fine_base[f + 1]);
+        // claim this warp's two tiles now: the CAS round trip overlaps the accumulation
+        uint32_t oc[2] = {0u, 0u};
+        if (lane == 0) {
+#pragma unroll
+            for (uint32_t kk = 0; kk < 2u; ++kk) {
+                const uint32_t t = f * (kFineBins / kTileBins) + warp + kk * (kPT / 32u);
+                if (t < p.n_tiles) {
+                    uint32_t* fl = p.tile_flags + t;
+                    oc[kk] = claim_outcome(fl, p.epoch, prev_word, atomicCAS(fl, prev_word, claimed_word));
+                }
+            }
+        }
         // accumulate (warp-strided 128-record steps, 4 per lane, coalesced)
         for (uint32_t base = r0 + warp * 128u; base < r1; base += (kPT / 32u) * 128u) {
             uint32_t key[4];
@@ -412,9 +432,17 @@ __global__ void __launch_bounds__(kPT, 1) k_part_bin(KernelParams p, PartArgs a)
             }
         }
         __syncthreads();
-        // flush the bucket's tiles with data: warp w takes tiles w, w + 16 (32 tiles of 256 bins)
-        for (uint32_t tt = warp; tt < kFineBins / kTileBins; tt += kPT / 32u) {
+        // flush: warp w owns tiles w and w + 16 of the bucket (claimed when the unit started); its
+        // won tiles go first (plain stores, then published), so a warp waits for a tile claimed
+        // elsewhere only when it holds nothing unpublished
+        const uint32_t oa = __shfl_sync(kFull, oc[0], 0), ob = __shfl_sync(kFull, oc[1], 0);
+        const bool swap = ob == kWon && oa != kWon;
+        for (uint32_t r = 0; r < 2u; ++r) {
+            const uint32_t kk = (r == 0u) == !swap ? 0u : 1u;
+            const uint32_t o = kk ? ob : oa;
+            const uint32_t tt = warp + kk * (kPT / 32u);
             const uint32_t t = f * (kFineBins / kTileBins) + tt;
+            if (o == 0u) continue;   // beyond the last tile
             uint32_t c[8][2], l[8][2], hh[8][2];
             bool nz = false;
 #pragma unroll
@@ -428,21 +456,18 @@ __global__ void __launch_bounds__(kPT, 1) k_part_bin(KernelParams p, PartArgs a)
                 *reinterpret_cast<uint2*>(s_lo + s) = make_uint2(0, 0);
                 *reinterpret_cast<uint2*>(s_hi + s) = make_uint2(0, 0);
             }
-            if (!__any_sync(kFull, nz) || t >= p.n_tiles) continue;
-            uint32_t won = 0;
-            if (lane == 0) {
-                uint32_t* fl = p.tile_flags + t;
-                const uint32_t o = claim_outcome(fl, p.epoch, prev_word, atomicCAS(fl, prev_word, claimed_word));
-                if (o == kBusy) {   // initialised by its claimer soon (it holds nothing we hold)
+            const bool won = o == kWon;
+            if (!won && !__any_sync(kFull, nz)) continue;   // nothing to add (a won tile is written even if empty)
+            if (o == kBusy) {   // claimed elsewhere: initialised after bounded work
+                if (lane == 0) {
                     uint32_t spins = 0;
-                    while (ld_acquire_u32(fl) != init_word) {
+                    while (ld_acquire_u32(p.tile_flags + t) != init_word) {
                         __nanosleep(200);
                         if (++spins > kSpinLimit) __trap();
                     }
                 }
-                won = o == kWon;
+                __syncwarp();
             }
-            won = __shfl_sync(kFull, won, 0);
             unsigned long long* g = p.bins + (size_t)t * kTileBins * 4u;
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
@@ -527,7 +552,7 @@ cudaError_t launch_partitioned(const KernelParams& p, void* scratch, const PartL
         default: SCAT(kTabGlobal) break;
     }
 #undef SCAT
-    k_part_fine<<<sm_count * 2, kPT, 0, st>>>(a);
+    k_part_fine<<<sm_count * 4, kPT, 0, st>>>(a);   // 4 x 26 KB smem, 32 registers: 4 CTAs per SM
     k_part_bin<<<sm_count, kPT, part_ring_smem(), st>>>(p, a);
     *launches += 5;
     return cudaGetLastError();
