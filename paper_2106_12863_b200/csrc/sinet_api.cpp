@@ -113,8 +113,6 @@ struct sinet_ctx {
     uint32_t stream_groups = 0;   // 0 auto, 1 or 2
     uint32_t stream_kernel = 0;   // 0 auto, 1 k_hist_stream (group barriers), 2 k_hist_ws (warp-specialised)
     uint32_t debug = 0;           // knob "debug_counters"
-    uint32_t block_threads = 0;   // knob "stream_threads"
-    uint32_t hot_agg = 0;         // knob "hot_agg"
     uint32_t shuffled_kernel = 0; // 0 auto (partition-then-bin when scratch is set), 1 L2 atomics only
     void* scratch = nullptr;      // caller scratch for the partitioned path (sinet_set_scratch)
     size_t scratch_bytes = 0;
@@ -193,8 +191,6 @@ KernelParams base_params(sinet_ctx* c) {
     p.stream_groups = c->stream_groups;
     p.stream_kernel = c->stream_kernel;
     p.debug = c->debug;
-    p.block_threads = c->block_threads;
-    p.hot_agg = c->hot_agg;
     p.ranges_per_group = c->ranges_per_group;
     p.pf_chunks = c->pf_chunks;
     p.range_counter = ws_u32(c, c->ws.counters);
@@ -1027,8 +1023,6 @@ int sinet_set_knob(sinet_ctx* c, const char* name, int64_t value) {
     else if (k == "stream_kernel" && range(0, 2)) c->stream_kernel = (uint32_t)value;
     else if (k == "shuffled_kernel" && range(0, 1)) c->shuffled_kernel = (uint32_t)value;
     else if (k == "debug_counters" && range(0, 1)) c->debug = (uint32_t)value;
-    else if (k == "stream_threads" && (value == 0 || value == 512 || value == 640)) c->block_threads = (uint32_t)value;
-    else if (k == "hot_agg" && range(0, 1)) c->hot_agg = (uint32_t)value;
     else if (k == "ranges_per_group" && range(0, 64)) c->ranges_per_group = (uint32_t)value;
     else if (k == "l2_prefetch_chunks" && range(0, 8)) c->pf_chunks = (uint32_t)value;
     else if (k == "table_mode" && range(-1, 3)) c->tab_mode = (int)value;

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     static_assert(NG == 1 || NG == 2, "one or two groups per CTA");
     constexpr uint32_t kHist = NT / 2 - 1;   // tiles of history kept below a chunk's newest tile
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ uint32_t s_red_all[NG][2][2][GW];
+    __shared__ __align__(16) uint32_t s_red_all[NG][2][2][GW];   // [group][parity][min, max][warp]
     __shared__ uint32_t s_state_all[NG][NT];   // (t+1) << 2 | claim outcome, per group
     __shared__ unsigned long long s_tot[(RPT == 2) ? 1 : NW * 12];
 
@@ -207,6 +207,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     // without a return value, the low word an atomic whose old value gives the exact carry.
     // Adds each taken record's high word (see accumulate) to hi[j].
     const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(s_win);
+    // Branch-free: EVERY record issues its two shared atomics, adding 0 when not taken (a
+    // predicated atomic in inline asm compiles to BSSY/BRA/BSYNC around each ATOMS -- 4-5
+    // instructions per atomic and a reconvergence point; measured in the C2 SASS).  The slot
+    // address is always inside the ring (dir & 1), and adding 0 changes nothing.
+    auto accumulate_all = [&](const bool (&take)[RPT], const uint32_t (&bin)[RPT], const uint32_t (&dir)[RPT],
+                              const uint64_t (&by)[RPT], uint32_t (&hi)[RPT]) {
+        uint32_t old[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const uint32_t a = win_base + ((bin[j] & (WS - 1)) * 2u + (dir[j] & 1u)) * 4u;
+            const uint32_t lo = take[j] ? (uint32_t)by[j] : 0u;
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(take[j] ? 1u : 0u) : "memory");
+            asm volatile("atom.shared.add.u32 %0, [%1+%3], %2;" : "=r"(old[j]) : "r"(a), "r"(lo), "n"(kLoOff * 4u) : "memory");
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const uint32_t lo = (uint32_t)by[j];
+            const uint32_t h = (uint32_t)(by[j] >> 32) + ((old[j] + lo < old[j]) ? 1u : 0u);
+            hi[j] += take[j] ? h : 0u;
+        }
+    };
     auto accumulate_n = [&](const bool (&take)[RPT], const uint32_t (&bin)[RPT], const uint32_t (&dir)[RPT],
                             const uint64_t (&by)[RPT], uint32_t (&hi)[RPT]) {
         uint32_t old[RPT];
@@ -331,24 +352,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
                 s_wtot[w][8] += o[0]; s_wtot[w][9] += o[1]; s_wtot[w][10] += o[2]; s_wtot[w][11] += o[3];
             }
         }
-        // Accumulate before the barrier every record whose tile is resident and neither being
-        // retired ([lo_t, act_t), claimed after the previous chunk) nor about to be recycled
-        // (>= lo_t + NT): retire only touches the slots of [lo_t, act_t).  Warps do this work
-        // instead of waiting at the barrier; the rest is accumulated after the retire.
+        // Accumulate before the barrier every record whose tile is resident ([lo_t, lo_t + NT),
+        // including the tiles claimed after the previous chunk, which retire right after the
+        // barrier); only records outside the ring are left for after the retire.
         uint32_t hi4[RPT];   // high words owed to HBM (added after the barrier)
 #pragma unroll
         for (int j = 0; j < RPT; ++j) hi4[j] = 0u;
-        // (knob hot_agg) a hot warp-chunk -- its first and last record in the same (bin, dir), a hot
-        // millisecond -- aggregates equal keys before the shared-memory atomics, which would
-        // otherwise serialise 32-way on one address
-        const bool hot = !kAgg && p.hot_agg && p.nbins < 0x40000000u &&
-                         __shfl_sync(kFull, dir4[0] < 2u ? (bin4[0] << 1) | dir4[0] : 0xFFFFFFFFu, 0) ==
-                             __shfl_sync(kFull, dir4[RPT - 1] < 2u ? (bin4[RPT - 1] << 1) | dir4[RPT - 1] : 0xFFFFFFFEu, 31);
-        if (!kAgg && have_window && !hot) {
+        if (!kAgg && have_window) {
             bool take[RPT];
 #pragma unroll
-            for (int j = 0; j < RPT; ++j) take[j] = dir4[j] < 2u && bin4[j] / kTileBins - act_t < lo_t + NT - act_t;
-            accumulate_n(take, bin4, dir4, cur.by, hi4);
+            for (int j = 0; j < RPT; ++j) take[j] = dir4[j] < 2u && bin4[j] / kTileBins - lo_t < NT;
+            accumulate_all(take, bin4, dir4, cur.by, hi4);
 #pragma unroll
             for (int j = 0; j < RPT; ++j) dir4[j] |= take[j] ? 4u : 0u;
         }
@@ -359,8 +373,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         group_sync();
         bmin = 0xFFFFFFFFu;
         bmax = 0u;
+        if constexpr (GW % 4 == 0) {   // 128-bit loads: GW/4 per array instead of GW scalar loads
 #pragma unroll
-        for (int w = 0; w < GW; ++w) { bmin = min(bmin, s_red[parity][0][w]); bmax = max(bmax, s_red[parity][1][w]); }
+            for (int w = 0; w < GW; w += 4) {
+                const uint4 a = *reinterpret_cast<const uint4*>(&s_red[parity][0][w]);
+                const uint4 b = *reinterpret_cast<const uint4*>(&s_red[parity][1][w]);
+                bmin = min(bmin, min(min(a.x, a.y), min(a.z, a.w)));
+                bmax = max(bmax, max(max(b.x, b.y), max(b.z, b.w)));
+            }
+        } else {
+            for (int w = 0; w < GW; ++w) { bmin = min(bmin, s_red[parity][0][w]); bmax = max(bmax, s_red[parity][1][w]); }
+        }
         const bool any = bmin <= bmax;
         const uint32_t bmin_t = bmin / kTileBins, bmax_t = bmax / kTileBins;
 
@@ -393,7 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         // ---- a6 (accumulate): reduce the chunk into the ring
         // the whole chunk inside the ring (the common case): no per-record residency/spill checks
         const bool all_in = any && bmin_t >= lo_t && bmax_t - lo_t < NT;
-        if (!kAgg && all_in && !hot) {
+        if (!kAgg && all_in) {
             bool rest[RPT];
             bool any_rest = false;
 #pragma unroll
@@ -419,7 +442,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
             // cheap neighbour test finds a duplicate in the warp (records of one slot are
             // RPT apart in stream order, so hot keys show up in adjacent lanes)
             bool try_agg = false;
-            if (kAgg || hot) {
+            if (kAgg) {
                 const uint32_t k32 = b ? ((bin4[j] << 1) | dir4[j]) : 0xFFFFFFFFu - lane;
                 const uint32_t kp = __shfl_up_sync(kFull, k32, 1);
                 try_agg = __any_sync(kFull, b && lane > 0u && kp == k32);
@@ -503,20 +526,9 @@ constexpr int kRingBins2 = 4096;
     k_hist_stream<512, G, (G == 1 ? kRingBins1 : kRingBins2), 4, A, W, S, WL>
 constexpr size_t kRingSmem = (size_t)kRingBins1 * 4u * 4u;   // 128 KB: 4 u32 per bin
 
-// experimental: 640 threads (2 groups of 10 warps), totals in shared memory (<= 102 registers)
-#define SINET_STREAM_KERNEL640(W, S) k_hist_stream<640, 2, kRingBins2, 4, false, W, S, false>
-
 cudaError_t setup_hist_stream() {
     const int mx = (int)(kRingSmem + kStreamTableSmem);
     cudaError_t e;
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(true, kTabByte), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(false, kTabByte), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(true, kTabPackedNoL2), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(SINET_STREAM_KERNEL640(false, kTabPackedNoL2), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
 #define SET(G, A, W, S, WL)                                                                                 \
     e = cudaFuncSetAttribute(SINET_STREAM_KERNEL(G, A, W, S, WL), cudaFuncAttributeMaxDynamicSharedMemorySize, mx); \
     if (e != cudaSuccess) return e;
@@ -553,16 +565,6 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
     cudaError_t e = cudaMemsetAsync(p.range_counter, 0, 8, st);
     if (e != cudaSuccess) return e;
-    if (p.block_threads == 640u && g == 2 && !agg && p.wn == 0u && (tab == kTabByte || tab == kTabPackedNoL2)) {
-        if (tab == kTabByte) {
-            if (w1) SINET_STREAM_KERNEL640(true, kTabByte)<<<grid, 640, sm, st>>>(q);
-            else SINET_STREAM_KERNEL640(false, kTabByte)<<<grid, 640, sm, st>>>(q);
-        } else {
-            if (w1) SINET_STREAM_KERNEL640(true, kTabPackedNoL2)<<<grid, 640, sm, st>>>(q);
-            else SINET_STREAM_KERNEL640(false, kTabPackedNoL2)<<<grid, 640, sm, st>>>(q);
-        }
-        return cudaGetLastError();
-    }
 #define LAUNCH(G, S, WL)                                                                                \
     if (agg && w1) SINET_STREAM_KERNEL(G, true, true, S, WL)<<<grid, 512, sm, st>>>(q);                  \
     else if (agg) SINET_STREAM_KERNEL(G, true, false, S, WL)<<<grid, 512, sm, st>>>(q);                  \

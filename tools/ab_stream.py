@@ -13,7 +13,7 @@ import paper_2106_12863_b200 as S  # noqa: E402
 from synth import WORKLOADS, prefix_table  # noqa: E402
 from synth.sinet_synth import records_into  # noqa: E402
 
-VARIANTS = [{}, {"stream_threads": 640}, {"hot_agg": 1}, {"stream_threads": 640, "hot_agg": 1}]
+VARIANTS = [{}]
 
 
 def timed(h, args, steps=10):

@@ -33,6 +33,7 @@ for s in "$@"; do
     pytest_new) timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 300 -k "ws or partitioned or bursty or gaps or dense or c1_full or table_enc or inline" > ${O}_pytest_new.txt 2>&1 ;;
     ncu_ws) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_ws -s 2 -c 1 -o ${O}_prof_ws python bench.py --steps 2 --warmup 1 --profile --knob stream_kernel=2 > ${O}_ncu_ws_run.txt 2>&1 ;;
     ncu_ws_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_ws -s 2 -c 1 -o ${O}_prof_ws_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile --knob stream_kernel=2 > ${O}_ncu_ws_c4_run.txt 2>&1 ;;
+    atomshuf) timeout 600 python bench.py --order shuffled --legs none --knob shuffled_kernel=1 --no-cpu --no-e2e --no-comparator --no-parse > ${O}_atomshuf.txt 2>&1 ;;
     benchshuf) timeout 1200 python bench.py --order shuffled --legs c4@shuffled --no-cpu --no-e2e --no-comparator --no-parse > ${O}_benchshuf.txt 2>&1 ;;
     benchws) timeout 1800 python bench.py --knob stream_kernel=2 > ${O}_benchws.txt 2>&1 ;;
     *) echo "unknown step $s" ;;
