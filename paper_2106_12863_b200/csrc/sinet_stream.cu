@@ -143,10 +143,37 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
         if (warp == 0u) my_o = o_l;
         const unsigned won_m = __ballot_sync(kFull, o_l == kWon), init_m = __ballot_sync(kFull, o_l == kInit);
         const bool busy = __any_sync(kFull, o_l == kBusy);
-        // pass 1: WON -> plain 128-bit stores, INIT -> RED.ADD; BUSY tiles keep their smem
-        for (unsigned m = won_m | init_m; m; m &= m - 1u) {
+        // pass 1a: WON tiles -> one 256-bit store per bin (no per-bin branch; the rare INIT tiles
+        // follow in their own loop).  A round covers TPR = GT / 256 tiles: thread tid takes bin
+        // tid % 256 of the round's (tid / 256)-th tile.
+        {
+            static_assert(GT % kTileBins == 0 && GT / kTileBins <= 2, "a round covers 1 or 2 tiles");
+            constexpr uint32_t TPR = GT / kTileBins;
+            const uint32_t sub = tid / kTileBins, i = tid % kTileBins;
+            for (unsigned m = won_m; m;) {
+                uint32_t k = (uint32_t)(__ffs(m) - 1);
+                m &= m - 1u;
+                bool ok = true;
+                if (TPR == 2) {   // the round's second tile (if any) goes to threads 256..511
+                    const uint32_t k1 = (uint32_t)(__ffs(m) - 1);
+                    if (sub) { ok = m != 0u; k = k1; }
+                    m &= m - 1u;
+                }
+                if (ok) {
+                    const uint32_t bin = (t_from + k) * kTileBins + i, s = bin & (WS - 1);
+                    uint2* sc = reinterpret_cast<uint2*>(s_win + s * 2u);
+                    uint2* sl = reinterpret_cast<uint2*>(s_win + kLoOff + s * 2u);
+                    const uint2 c = *sc, l = *sl;   // {cnt_out, cnt_in}, {lo_out, lo_in}
+                    *sc = make_uint2(0u, 0u);
+                    *sl = make_uint2(0u, 0u);
+                    st_cs_v4u64(p.bins + (size_t)bin * 4u, c.x, l.x, c.y, l.y);
+                }
+            }
+        }
+        // pass 1b: INIT tiles (another CTA initialised them: rare) -> RED.ADD
+        for (unsigned m = init_m; m; m &= m - 1u) {
             const uint32_t k = (uint32_t)(__ffs(m) - 1);
-            for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin((t_from + k) * kTileBins + i, (won_m >> k) & 1u);
+            for (uint32_t i = tid; i < kTileBins; i += GT) flush_bin((t_from + k) * kTileBins + i, false);
         }
         group_sync();
         // pass 2: publish WON tiles; wait (holding nothing unreleased) for BUSY ones

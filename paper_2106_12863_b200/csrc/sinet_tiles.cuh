@@ -53,6 +53,13 @@ __device__ __forceinline__ void prefetch_records(const KernelParams& p, uint64_t
     prefetch_l2(p.bytes + a, (uint32_t)(n * 8));
 }
 
+// One 32-byte bin {a, b, c, d} (u64 each, from u32 values) with a single 256-bit evict-first
+// store (STG.E.EF.256, sm_100): the bins are written once and never re-read by the kernel.
+__device__ __forceinline__ void st_cs_v4u64(unsigned long long* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"((unsigned long long)a),
+                 "l"((unsigned long long)b), "l"((unsigned long long)c), "l"((unsigned long long)d) : "memory");
+}
+
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
