@@ -118,7 +118,6 @@ struct sinet_ctx {
     size_t scratch_bytes = 0;
     uint64_t scratch_cap = 0;     // records per partitioned sub-batch
     uint32_t ranges_per_group = 0;
-    uint32_t pf_chunks = 0;           // L2 bulk prefetch distance (measured: off is fastest, C2 1.43 vs 1.46 ms)
     int tab_mode = -1;            // stream kernel lookup-table encoding: -1 automatic, 0..3 forced
     int exchange = 0;             // multi-GPU merge: 0 auto (sparse when cheaper), 1 dense, 2 sparse
     int last_exchange = 0;        // 1 dense reduce-scatter, 2 sparse touched-range exchange
@@ -192,7 +191,6 @@ KernelParams base_params(sinet_ctx* c) {
     p.stream_kernel = c->stream_kernel;
     p.debug = c->debug;
     p.ranges_per_group = c->ranges_per_group;
-    p.pf_chunks = c->pf_chunks;
     p.range_counter = ws_u32(c, c->ws.counters);
     p.touched = ws_u32(c, c->ws.counters) + 4;
     p.wbits = c->wbits;
@@ -1024,7 +1022,6 @@ int sinet_set_knob(sinet_ctx* c, const char* name, int64_t value) {
     else if (k == "shuffled_kernel" && range(0, 1)) c->shuffled_kernel = (uint32_t)value;
     else if (k == "debug_counters" && range(0, 1)) c->debug = (uint32_t)value;
     else if (k == "ranges_per_group" && range(0, 64)) c->ranges_per_group = (uint32_t)value;
-    else if (k == "l2_prefetch_chunks" && range(0, 8)) c->pf_chunks = (uint32_t)value;
     else if (k == "table_mode" && range(-1, 3)) c->tab_mode = (int)value;
     else if (k == "exchange" && range(0, 2)) c->exchange = (int)value;
     else return fail(c, SINET_E_INVAL, "unknown knob or value out of range: " + k);

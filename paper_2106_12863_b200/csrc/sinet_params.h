@@ -45,7 +45,6 @@ struct KernelParams {
     uint32_t stream_groups;        // 0 auto, 1 or 2: layout of the stream kernel's ring
     uint32_t stream_kernel;        // 0 auto, 1 group-barrier kernel (k_hist_stream), 2 warp-specialised (k_hist_ws)
     uint32_t debug;                // 1: k_hist_ws counts its slow paths (sinet_debug_counters)
-    uint32_t pf_chunks;            // stream kernel: L2 bulk-prefetch distance in chunks (0 = off)
     uint32_t ranges_per_group;     // 0 = default: record ranges handed out per group (load balance)
     uint32_t n_ranges;             // set by the launcher
     uint32_t* range_counter;       // zeroed by the launcher before each launch

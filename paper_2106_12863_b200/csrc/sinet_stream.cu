@@ -293,25 +293,57 @@ __global__ void __launch_bounds__(THREADS, 1) k_hist_stream(KernelParams p) {
     const uint64_t r0 = (ngroups * range / nranges) * 4, r1 = (ngroups * (range + 1) / nranges) * 4;
     lo_t = 0; act_t = 0; have_window = false; hull_lo = 0xFFFFFFFFu; hull_hi = 0u;
 
-    // chunks whose every record is valid: not the batch's ragged first/last 4-record group
+    // Chunk k of the range covers virtual records [r0 + k CH, r0 + (k+1) CH); all per-chunk
+    // bounds are precomputed per range as 32-bit chunk indices (no 64-bit compares per chunk).
+    constexpr uint32_t CH = (uint32_t)GT * RPT;   // records per chunk
+    const uint32_t span = (uint32_t)(r1 - r0);     // < 2^31 (launch_hist_stream)
+    const uint32_t nch = (span + CH - 1u) / CH;
+    const uint32_t off = tid * (uint32_t)RPT;      // this thread's first record in a chunk
+    // chunks where this thread has records: r0 + k CH + off < r1
+    const uint32_t nhave = span > off ? (span - off + CH - 1u) / CH : 0u;
+    // chunks whose every record is valid (not the batch's ragged first/last 4-record group)
     const uint64_t full_lo = (p.head != 0u) ? 4u : 0u;
     const uint64_t full_hi = (r1 > p.nv) ? r1 - 4 : r1;
-    constexpr uint64_t CH = (uint64_t)GT * RPT;   // records per chunk
+    const uint32_t kf0 = r0 < full_lo ? 1u : 0u;
+    const uint32_t kf1 = (uint32_t)((full_hi - r0) / CH);
+    // chunks where this thread's 4 records are one 16-byte group of every column (128-bit loads)
+    const uint64_t g0 = r0 + off;
+    const uint32_t kv0 = g0 < p.head ? 1u : 0u;
+    const uint32_t kv1 = p.nv >= g0 + RPT ? (uint32_t)((p.nv - g0 - RPT) / CH) + 1u : 0u;
+    // column pointers of this thread's group in chunk 0 (may point before the column: only
+    // dereferenced for chunks in [kv0, kv1))
+    const int64_t e0 = (int64_t)g0 - (int64_t)p.head;
+    const uint64_t* ts_b = p.ts + e0;
+    const uint32_t* src_b = p.src + e0;
+    const uint32_t* dst_b = p.dst + e0;
+    const uint64_t* by_b = p.bytes + e0;
+    auto load_chunk = [&](uint32_t k, Rec& r) {
+        if constexpr (RPT == 4) {
+            if (k >= kv0 && k < kv1) {
+                const uint32_t a = k * CH;
+                const ulonglong2 t0 = ldcs_v2u64(ts_b + a), t1 = ldcs_v2u64(ts_b + a + 2);
+                const uint4 sv = ldcs_v4u32(src_b + a), dv = ldcs_v4u32(dst_b + a);
+                const ulonglong2 b0 = ldcs_v2u64(by_b + a), b1 = ldcs_v2u64(by_b + a + 2);
+                r.ts[0] = t0.x; r.ts[1] = t0.y; r.ts[2] = t1.x; r.ts[3] = t1.y;
+                r.src[0] = sv.x; r.src[1] = sv.y; r.src[2] = sv.z; r.src[3] = sv.w;
+                r.dst[0] = dv.x; r.dst[1] = dv.y; r.dst[2] = dv.z; r.dst[3] = dv.w;
+                r.by[0] = b0.x; r.by[1] = b0.y; r.by[2] = b1.x; r.by[3] = b1.y;
+                return;
+            }
+        }
+        loadN<RPT>(p, g0 + (uint64_t)k * CH, r);
+    };
     Rec cur, nxt;
-    const uint64_t kPF = p.pf_chunks;   // L2 prefetch distance in chunks (0: off)
-    if (tid == 0 && kPF > 1) prefetch_records(p, r0 + CH, min(r0 + kPF * CH, r1));
-    if (r0 + (uint64_t)tid * RPT < r1) loadN<RPT>(p, r0 + (uint64_t)tid * RPT, cur);
+    if (nhave) load_chunk(0u, cur);
     uint32_t parity = 0;
 
-    for (uint64_t cbase = r0; cbase < r1; cbase += CH, parity ^= 1u) {
-        const uint64_t my_v = cbase + (uint64_t)tid * RPT;   // this thread's first record
-        const bool have = my_v < r1;
+    for (uint32_t k = 0; k < nch; ++k, parity ^= 1u) {
+        const uint64_t my_v = g0 + (uint64_t)k * CH;   // this thread's first record (general path only)
+        const bool have = k < nhave;
         // every record of the chunk valid (all but the batch's ragged ends): no per-record checks
-        const bool full = cbase >= full_lo && cbase + CH <= full_hi;
+        const bool full = k >= kf0 && k < kf1;
         const bool tags_on = p.tags != nullptr;
-        if (my_v + CH < r1) loadN<RPT>(p, my_v + CH, nxt);   // prefetch into registers
-        // keep more bytes in flight than one chunk of registers: the chunks kPF ahead go to L2
-        if (tid == 0 && kPF && cbase + kPF * CH < r1) prefetch_records(p, cbase + kPF * CH, min(cbase + (kPF + 1) * CH, r1));
+        if (k + 1u < nhave) load_chunk(k + 1u, nxt);   // prefetch into registers
 
         // ---- a3-a5: classify and map this chunk (the claims issued last chunk resolve meanwhile)
         // dir4[j]: 0 / 1 = the record is binned in that direction and still to be accumulated,
@@ -590,6 +622,8 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 4u);
     const uint64_t max_r = p.nv / (4u * 512u * 4u) + 1u;
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
+    // a range spans < 2^31 records (the kernel indexes chunks of a range in 32 bits)
+    if ((uint64_t)q.n_ranges < (p.nv >> 30) + 1u) q.n_ranges = (uint32_t)((p.nv >> 30) + 1u);
     cudaError_t e = cudaMemsetAsync(p.range_counter, 0, 8, st);
     if (e != cudaSuccess) return e;
 #define LAUNCH(G, S, WL)                                                                                \

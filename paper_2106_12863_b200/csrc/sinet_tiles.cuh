@@ -34,25 +34,6 @@ __device__ __forceinline__ uint32_t smem_count_and_add_lo(uint32_t a, bool take,
     return old;
 }
 
-// TMA bulk prefetch of [ptr, ptr + bytes) into L2 (16-byte aligned, multiple of 16; a hint)
-__device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
-    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
-}
-
-// Prefetch the four columns of virtual records [v0, v1) into L2 (clamped to the batch).
-__device__ __forceinline__ void prefetch_records(const KernelParams& p, uint64_t v0, uint64_t v1) {
-    if (v0 < p.head) v0 = p.head;
-    if (v1 > p.nv) v1 = p.nv;
-    v0 = (v0 + 3) & ~3ull;   // whole 16-byte groups only (the virtual index is 16-byte aligned per 4)
-    v1 &= ~3ull;
-    if (v1 <= v0) return;
-    const uint64_t a = v0 - p.head, n = v1 - v0;
-    prefetch_l2(p.ts + a, (uint32_t)(n * 8));
-    prefetch_l2(p.src + a, (uint32_t)(n * 4));
-    prefetch_l2(p.dst + a, (uint32_t)(n * 4));
-    prefetch_l2(p.bytes + a, (uint32_t)(n * 8));
-}
-
 // One 32-byte bin {a, b, c, d} (u64 each, from u32 values) with a single 256-bit evict-first
 // store (STG.E.EF.256, sm_100): the bins are written once and never re-read by the kernel.
 __device__ __forceinline__ void st_cs_v4u64(unsigned long long* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {

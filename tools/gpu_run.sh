@@ -19,6 +19,9 @@ for s in "$@"; do
     bench) timeout 1200 python bench.py > ${O}_bench.txt 2>&1 ;;
     ref) timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > ${O}_ref.txt 2>&1 ;;
     c1|c2|c3|c4|c5) $B --config $s > ${O}_$s.txt 2>&1 ;;
+    var_*) # var_NAME_CFG: the same bench line with libsinet.NAME.so (tools/build_variant.py)
+      v=${s#var_}; name=${v%_*}; cfg=${v##*_}
+      SINET_LIB_VARIANT=$name $B --config $cfg > ${O}_$s.txt 2>&1 ;;
     shuf) $B --order shuffled > ${O}_shuf.txt 2>&1 ;;
     shuf_c4) $B --config c4 --order shuffled > ${O}_shuf_c4.txt 2>&1 ;;
     launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_run.txt 2>&1 ;;
