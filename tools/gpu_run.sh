@@ -19,6 +19,9 @@ for s in "$@"; do
     bench) timeout 1200 python bench.py > ${O}_bench.txt 2>&1 ;;
     ref) timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > ${O}_ref.txt 2>&1 ;;
     c1|c2|c3|c4|c5) $B --config $s > ${O}_$s.txt 2>&1 ;;
+    knob_*) # knob_NAME=VALUE_CFG: the bench line with one sinet_set_knob setting
+      v=${s#knob_}; kv=${v%_*}; cfg=${v##*_}
+      $B --config $cfg --knob $kv > ${O}_$s.txt 2>&1 ;;
     var_*) # var_NAME_CFG: the same bench line with libsinet.NAME.so (tools/build_variant.py)
       v=${s#var_}; name=${v%_*}; cfg=${v##*_}
       SINET_LIB_VARIANT=$name $B --config $cfg > ${O}_$s.txt 2>&1 ;;
