@@ -616,10 +616,18 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     const int g = stream_groups_for(p);
     KernelParams q = p;
     // record ranges handed out dynamically, a whole number per group (a partial last wave
-    // leaves most groups idle: C2 with 625 ranges 1.72 ms vs 592 = 2 per group 1.36 ms).
-    // Measured per group: 2 -> C2 1.36 / C4@400M 4.95 / 4 -> 1.37 / 4.39 / 8 -> 1.41 / 4.09 ms
-    // (long ranges save window warm-up and drain, short ones balance bursty stretches): 4.
-    const uint64_t per = (uint64_t)grid * (uint64_t)g * (uint64_t)(p.ranges_per_group ? p.ranges_per_group : 4u);
+    // leaves most groups idle: C2 with 625 ranges 1.72 ms vs 592 = 2 per group 1.36 ms), each
+    // about kRangeRecords long: long ranges save window warm-up and drain (the boundary tiles
+    // of a range are shared with its neighbours: RED instead of plain stores), short ones
+    // balance bursty stretches.  Measured ranges per group (C2 100 M / C4 1.6 B bursty / C5
+    // 400 M, ms): 2 -> 1.211 / - / -, 4 -> 1.217 / 12.87 / 4.78, 8 -> 1.246 / 12.53 / 4.81,
+    // 16 -> - / 12.25 / 4.93, 32 -> - / 12.15 / -: ~170-340 k records per range is best for
+    // all three.
+    constexpr uint64_t kRangeRecords = 200000;
+    const uint64_t groups_total = (uint64_t)grid * (uint64_t)g;
+    const uint64_t rpg = p.ranges_per_group ? p.ranges_per_group
+                                            : (p.nv + groups_total * kRangeRecords / 2) / (groups_total * kRangeRecords);
+    const uint64_t per = groups_total * (rpg ? rpg : 1u);
     const uint64_t max_r = p.nv / (4u * 512u * 4u) + 1u;
     q.n_ranges = (uint32_t)(per < max_r ? per : max_r);
     // a range spans < 2^31 records (the kernel indexes chunks of a range in 32 bits)
