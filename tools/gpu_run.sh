@@ -10,6 +10,14 @@ O=gpurun_out/${TAG}
 python -c "import paper_2106_12863_b200" || exit 1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > ${O}_gpu.txt 2>&1
 lscpu > ${O}_lscpu.txt 2>&1
+# ncu reports are large (gpurun returns <= 64 MiB): keep CSV exports of the counters, the
+# per-instruction source view and the details page, drop the .ncu-rep
+export_rep() {
+  ncu -i $1.ncu-rep --page raw --csv > $1_raw.csv 2>&1
+  ncu -i $1.ncu-rep --page source --csv --print-source=sass > $1_src.csv 2>&1
+  ncu -i $1.ncu-rep --page details > $1_details.txt 2>&1
+  rm -f $1.ncu-rep
+}
 B="timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse"
 for s in "$@"; do
   case $s in
@@ -30,9 +38,9 @@ for s in "$@"; do
     launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_run.txt 2>&1 ;;
     launches_shuf) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file ${O}_launches_shuf.csv python bench.py --order shuffled --steps 2 --warmup 3 --legs none --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_shuf_run.txt 2>&1 ;;
     ncu_part) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_part -s 5 -c 5 -o ${O}_prof_part python bench.py --order shuffled --steps 1 --warmup 1 --profile > ${O}_ncu_part_run.txt 2>&1 ;;
-    ncu_c2) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c2 python bench.py --steps 2 --warmup 1 --profile > ${O}_ncu_c2_run.txt 2>&1 ;;
-    ncu_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile > ${O}_ncu_c4_run.txt 2>&1 ;;
-    ncu_c5) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c5 python bench.py --config c5 --steps 2 --warmup 1 --profile > ${O}_ncu_c5_run.txt 2>&1 ;;
+    ncu_c2) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c2 python bench.py --steps 2 --warmup 1 --profile > ${O}_ncu_c2_run.txt 2>&1; export_rep ${O}_prof_c2 ;;
+    ncu_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile > ${O}_ncu_c4_run.txt 2>&1; export_rep ${O}_prof_c4 ;;
+    ncu_c5) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c5 python bench.py --config c5 --steps 2 --warmup 1 --profile > ${O}_ncu_c5_run.txt 2>&1; export_rep ${O}_prof_c5 ;;
     san) for t in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $t python tools/sanitize_case.py > ${O}_san_$t.txt 2>&1; done ;;
     wscheck) timeout 400 python tools/ws_check.py > ${O}_wscheck.txt 2>&1 ;;
     ab) timeout 900 python tools/ab_stream.py > ${O}_ab.txt 2>&1 ;;

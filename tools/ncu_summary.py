@@ -3,6 +3,7 @@
 
   python tools/ncu_summary.py launches gpurun_out/launches.csv        -> per-kernel share of device time
   python tools/ncu_summary.py full gpurun_out/prof_stream.ncu-rep     -> key counters of the captured kernel
+  python tools/ncu_summary.py full gpurun_out/prof_stream_raw.csv     -> the same from its --page raw --csv export
 """
 import csv
 import io
@@ -41,8 +42,13 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.check_output(["ncu", "-i", path, "--page", "raw", "--csv"], text=True)
+    # an .ncu-rep, or the `--page raw --csv` export of one (tools/gpu_run.sh keeps only that)
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.check_output(["ncu", "-i", path, "--page", "raw", "--csv"], text=True)
     rows = list(csv.reader(io.StringIO(out)))
+    rows = rows[next(i for i, r in enumerate(rows) if "Kernel Name" in r or "ID" in r[:2]):]
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
