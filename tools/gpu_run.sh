@@ -35,9 +35,9 @@ for s in "$@"; do
       SINET_LIB_VARIANT=$name $B --config $cfg > ${O}_$s.txt 2>&1 ;;
     shuf) $B --order shuffled > ${O}_shuf.txt 2>&1 ;;
     shuf_c4) $B --config c4 --order shuffled > ${O}_shuf_c4.txt 2>&1 ;;
-    launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_run.txt 2>&1 ;;
-    launches_shuf) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file ${O}_launches_shuf.csv python bench.py --order shuffled --steps 2 --warmup 3 --legs none --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_shuf_run.txt 2>&1 ;;
-    ncu_part) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_part -s 5 -c 5 -o ${O}_prof_part python bench.py --order shuffled --steps 1 --warmup 1 --profile > ${O}_ncu_part_run.txt 2>&1 ;;
+    launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_run.txt 2>&1 ;;
+    launches_shuf) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 200 --csv --log-file ${O}_launches_shuf.csv python bench.py --order shuffled --steps 2 --warmup 3 --legs none --no-cpu --no-e2e --no-comparator --no-parse > ${O}_launches_shuf_run.txt 2>&1 ;;
+    ncu_part) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_part -s 5 -c 5 -o ${O}_prof_part python bench.py --order shuffled --steps 1 --warmup 1 --profile > ${O}_ncu_part_run.txt 2>&1; for f in ${O}_prof_part*.ncu-rep; do export_rep ${f%.ncu-rep}; done ;;
     ncu_c2) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c2 python bench.py --steps 2 --warmup 1 --profile > ${O}_ncu_c2_run.txt 2>&1; export_rep ${O}_prof_c2 ;;
     ncu_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile > ${O}_ncu_c4_run.txt 2>&1; export_rep ${O}_prof_c4 ;;
     ncu_c5) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_stream -s 2 -c 1 -o ${O}_prof_c5 python bench.py --config c5 --steps 2 --warmup 1 --profile > ${O}_ncu_c5_run.txt 2>&1; export_rep ${O}_prof_c5 ;;
