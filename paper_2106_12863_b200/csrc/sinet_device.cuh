@@ -173,17 +173,24 @@ __device__ __forceinline__ void member_batch_nol2(const uint32_t (&ip)[K], uint3
         // and the low half of .w, the parity of the boundaries before the block at .w bit 16,
         // .w bit 31 = more than 7 boundaries (.x = its mentry: search).  Branch-free: a warp holds
         // 256 addresses, so a rare loop-carrying path would run in nearly every warp.
-        auto below = [](uint32_t w, uint32_t x) {   // #u16 halves of w below x
-            return ((w & 0xFFFFu) < x ? 1u : 0u) + ((w >> 16) < x ? 1u : 0u);
-        };
+        // The entry's 7 u16 values are sorted (a block's boundaries ascend; unused slots are
+        // 0xFFFF), so #values below x is a 3-step branch-free binary search over them (with an
+        // implicit +inf eighth slot), and the count's parity is the last step's outcome: 3
+        // compares and 3 selects instead of 7 compares and 7 adds (C5: the linear decode was 65
+        // of 242 instructions per record).
         const uint4* me128 = reinterpret_cast<const uint4*>(T.mentry);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             if (c[k] != 2u) continue;
             const uint4 e = me128[r[k]];
             const uint32_t x = ip[k] & 0xFFFFu;
-            const uint32_t cnt = below(e.x, x) + below(e.y, x) + below(e.z, x) + ((e.w & 0xFFFFu) < x ? 1u : 0u);
-            in[k] = (cnt ^ (e.w >> 16)) & 1u;
+            const uint32_t v0 = e.x & 0xFFFFu, v1 = e.x >> 16, v2 = e.y & 0xFFFFu, v3 = e.y >> 16;
+            const uint32_t v4 = e.z & 0xFFFFu, v5 = e.z >> 16, v6 = e.w & 0xFFFFu;
+            const bool p1 = v3 < x;                       // count >= 4
+            const bool p2 = (p1 ? v5 : v1) < x;           // count >= base + 2
+            const bool p3 = (p1 ? (p2 ? v6 : v4) : (p2 ? v2 : v0)) < x;
+            // count = 4 p1 + 2 p2 + p3: its parity is p3
+            in[k] = ((p3 ? 1u : 0u) ^ (e.w >> 16)) & 1u;
         }
         if (T.any_long) {   // CTA-uniform: the list has a mixed /16 with more than 7 boundaries
 #pragma unroll
