@@ -321,9 +321,13 @@ __global__ void __launch_bounds__(kPT) k_part_fine(PartArgs a) {
     for (;;) {
         if (threadIdx.x == 0) s_u = atomicAdd(&a.counters[0], 1u);
         __syncthreads();
-        const uint32_t u = s_u;
+        const uint32_t ticket = s_u;
         __syncthreads();
-        if (u >= n_units) break;
+        if (ticket >= n_units) break;
+        // tickets are spread over the coarse buckets (u = ticket * P mod n_units, P a prime
+        // larger than any unit count: a bijection): consecutive units of one coarse bucket would
+        // have every CTA reserve space on the same 128 fine cursors at once
+        const uint32_t u = (uint32_t)(((uint64_t)ticket * 982451653ull) % n_units);
         // coarse bucket of unit u: the last c with cunit_base[c] <= u
         uint32_t lo = 0, len = a.nc;
         while (len) {

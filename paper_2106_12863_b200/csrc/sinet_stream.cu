@@ -12,9 +12,9 @@
 //   * count and bytes are accumulated with native shared-memory u32 atomics
 //     (bytes as lo/hi words with an exact carry), equal keys of a warp are
 //     aggregated first (hot bins);
-//   * when the window slides past a 512-bin tile, the tile is retired to HBM
+//   * when the window slides past a 256-bin tile, the tile is retired to HBM
 //     exactly once: the first CTA to claim it (state word CAS) stores its bins
-//     with plain 128-bit stores (no memset, no read-modify-write), later
+//     with one 256-bit store each (no memset, no read-modify-write), later
 //     contributors wait until it is initialised and add with RED.ADD.64.
 // Records outside the window (late beyond the window, or a chunk wider than
 // it) take the same claim-then-RED path one at a time, so the result is exact
@@ -32,8 +32,8 @@ namespace sinet {
 // a warp's 32 records spread over all 32 banks (16 with one 16-byte slot per bin).  A record whose bytes
 // reach the high word (>= 2^32, or a carry out of the low word: elephants, very hot bins)
 // adds that part straight to HBM through the spill path, after the chunk barrier, when
-// the group holds no claim.  A thread retires one bin as one full 32-byte sector, so a
-// warp writes 1 KB contiguous per store pair.  Tiles [lo_t, lo_t + NT)
+// the group holds no claim.  A thread retires one bin as one full 32-byte sector (one
+// STG.E.EF.256), so a warp writes 1 KB contiguous per store.  Tiles [lo_t, lo_t + NT)
 // are resident.  After a chunk is accumulated, tiles below the chunk's
 // oldest bin (keeping >= NT/2-1 tiles of history) are claimed with one
 // non-blocking CAS each; the CAS resolves while the next chunk is loaded and
