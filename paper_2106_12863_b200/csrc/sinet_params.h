@@ -30,7 +30,6 @@ struct KernelParams {
     unsigned long long* totals;    // 12 x u64
     uint32_t* tile_flags;          // [n_tiles]
     const uint32_t* cls2;          // [4096]
-    const uint32_t* entry;         // [65536]
     const uint32_t* bnd;           // [nbnd]
     const uint32_t* rank;          // [2048] u16 pairs: mixed blocks before each class-table word
     const uint32_t* mentry;        // [n_mixed] entry of each mixed /16 block
