@@ -189,6 +189,29 @@ def test_dense_stream_both_layouts(S, oracle_lib, groups):
                                                              wl.window_start_ms, wl.window_ms))
 
 
+@pytest.mark.parametrize("rpg", [0, 1, 64])
+@pytest.mark.parametrize("groups", [1, 2])
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_range_count_and_retire_parity(S, oracle_lib, name, groups, rpg):
+    """Record ranges per ring group: automatic (~200 k records), one, and 64 (ranges of a few
+    thousand records: many shared boundary tiles, initialised-by-another-CTA retires) over the
+    dense uniform and the bursty shape, both ring layouts (one 512-thread group retires two
+    tiles per round)."""
+    wl = WORKLOADS[name].with_(n=6_000_000, window_ms=3_600_000)
+    nets, lens = prefix_table(wl)
+    cols = to_numpy(records(wl))
+    o = oracle_lib.classify_histogram(*cols, nets, lens, wl.window_start_ms, wl.window_ms, 1, threads=8)
+    h = S.SinetHistogram(nets, lens, wl.window_start_ms, wl.window_ms, 1, order=1)
+    h.set_knob("stream_kernel", 1)
+    h.set_tuning(groups, -1)
+    h.set_knob("ranges_per_group", rpg)
+    h.classify(*dev_cols(cols))
+    g = {"count": np.stack([h.read_bins(k, S.METRIC_COUNT) for k in (0, 1)]),
+         "bytes": np.stack([h.read_bins(k, S.METRIC_BYTES) for k in (0, 1)]), "totals": h.read_totals()}
+    h.close()
+    assert_parity(g, o)
+
+
 @pytest.mark.parametrize("strategy,groups", [(1, 1), (1, 2), (1, "ws"), (2, 0)])
 def test_bursty_hot_bins(S, oracle_lib, strategy, groups):
     """C4-shaped (diurnal + Zipf bursts + 1 % in one ms) and a degenerate all-in-one-ms batch."""

@@ -50,6 +50,7 @@ for s in "$@"; do
     ab) timeout 900 python tools/ab_stream.py > ${O}_ab.txt 2>&1 ;;
     pytest_stream) timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 300 -k "not ws and (test_adversarial_parity or table_enc or inline or dense or bursty or gaps or c1_full or chunked or watchlist or (full_size_digest and stream))" > ${O}_pytest_stream.txt 2>&1 ;;
     pytest_part) timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 300 -k "partitioned or (full_size_digest and shuffled and (c1 or c2 or c5))" > ${O}_pytest_part.txt 2>&1 ;;
+    pytest_range) timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 300 -k "range_count" > ${O}_pytest_range.txt 2>&1 ;;
     pytest_new) timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 300 -k "ws or partitioned or bursty or gaps or dense or c1_full or table_enc or inline" > ${O}_pytest_new.txt 2>&1 ;;
     ncu_ws) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_ws -s 2 -c 1 -o ${O}_prof_ws python bench.py --steps 2 --warmup 1 --profile --knob stream_kernel=2 > ${O}_ncu_ws_run.txt 2>&1 ;;
     ncu_ws_c4) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist_ws -s 2 -c 1 -o ${O}_prof_ws_c4 python bench.py --config c4 --steps 2 --warmup 1 --profile --knob stream_kernel=2 > ${O}_ncu_ws_c4_run.txt 2>&1 ;;
