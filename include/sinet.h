@@ -393,7 +393,7 @@ int sinet_table_member_host_labelled(const uint32_t* prefix_net, const uint8_t* 
 int sinet_set_tuning(sinet_ctx* ctx, int stream_groups, int warp_aggregation);
 /* Named performance knobs (results are identical for every setting; they exist for A/B
  * measurements and tests): "stream_groups" 0..2, "warp_aggregation" 0/1,
- * "ranges_per_group" 0..64 (0 = default: ranges of ~200 k records), "table_mode" -1..3
+ * "ranges_per_group" 0..64 (0 = default: ranges of ~300 k records), "table_mode" -1..3
  * (as sinet_set_table_mode), "exchange" 0..2 (as sinet_set_exchange), "stream_kernel" 0..2
  * (0 automatic, 1 the group-barrier kernel k_hist_stream, 2 the warp-specialised k_hist_ws),
  * "shuffled_kernel" 0..1 (0 partition-then-bin when scratch is registered, 1 L2 atomics).

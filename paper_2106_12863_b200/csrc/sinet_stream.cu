@@ -621,9 +621,10 @@ cudaError_t launch_hist_stream(const KernelParams& p, int sm_count, bool agg, cu
     // of a range are shared with its neighbours: RED instead of plain stores), short ones
     // balance bursty stretches.  Measured ranges per group (C2 100 M / C4 1.6 B bursty / C5
     // 400 M, ms): 2 -> 1.211 / - / -, 4 -> 1.217 / 12.87 / 4.78, 8 -> 1.246 / 12.53 / 4.81,
-    // 16 -> - / 12.25 / 4.93, 32 -> - / 12.15 / -: ~170-340 k records per range is best for
-    // all three.
-    constexpr uint64_t kRangeRecords = 200000;
+    // 16 -> - / 12.25 / 4.93, 32 -> - / 12.15 / -; C2 at 1 per group (338 k) 1.200, C3 1.2 B
+    // at 10 / 20 per group 9.065 / 9.121: uniform input prefers ~300-400 k records per range,
+    // bursty ~170 k (within 1 %): 300 k.
+    constexpr uint64_t kRangeRecords = 300000;
     const uint64_t groups_total = (uint64_t)grid * (uint64_t)g;
     const uint64_t rpg = p.ranges_per_group ? p.ranges_per_group
                                             : (p.nv + groups_total * kRangeRecords / 2) / (groups_total * kRangeRecords);

@@ -193,7 +193,7 @@ def test_dense_stream_both_layouts(S, oracle_lib, groups):
 @pytest.mark.parametrize("groups", [1, 2])
 @pytest.mark.parametrize("name", ["c2", "c4"])
 def test_range_count_and_retire_parity(S, oracle_lib, name, groups, rpg):
-    """Record ranges per ring group: automatic (~200 k records), one, and 64 (ranges of a few
+    """Record ranges per ring group: automatic (~300 k records), one, and 64 (ranges of a few
     thousand records: many shared boundary tiles, initialised-by-another-CTA retires) over the
     dense uniform and the bursty shape, both ring layouts (one 512-thread group retires two
     tiles per round)."""
